@@ -1,0 +1,266 @@
+/*
+ * dattn.h -- C ABI of the B200-native DistAttention decode path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or C++
+ * types. It follows the conventions of the reference's C ABI
+ * (/root/reference/proj/include/kvsched.h:1-32): every call returns a status,
+ * a message for the last failure of the calling thread is in
+ * dattn_last_error(), out-pointers are written only on success, strings
+ * returned through char** are freed with dattn_string_free().
+ *
+ * Each entry point cites the reference interface it replaces. The reference's
+ * hot path is the C++ operator API kvsched::attn
+ * (proj/include/kvsched/distattention.hpp:16-95); the C++ mirror of that API
+ * (include/dattn_kvsched.hpp, paper_2401_02669_b200/csrc/kvsched_adapter.cpp)
+ * is implemented on top of these calls.
+ *
+ * Device layout:
+ *   K pool, V pool : [num_pages][num_kv_heads][page_tokens][padded_dim]  (dtype)
+ *   block tables   : int32 [max_seqs][max_pages_per_seq]
+ *   queries        : [rows][num_q_heads][padded_dim]                     (dtype)
+ *   outputs        : [rows][num_q_heads][padded_dim]                     (dtype)
+ *   partial record : [m, e, tokens, 0, ma[padded_dim]]  (fp32; fp64 for F64 stores)
+ *
+ * Threading: a store is used by one host thread at a time (one store per
+ * GPU / stream); different stores are independent.
+ */
+#ifndef DATTN_H
+#define DATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* kvsched.h:20-26 plus device-side codes. */
+typedef enum dattn_status {
+    DATTN_OK = 0,
+    DATTN_ERR_INVALID_ARGUMENT = 1, /* null pointers, malformed parameters */
+    DATTN_ERR_INPUT = 2,            /* rejected data: non-finite values, bad payloads */
+    DATTN_ERR_CONTRACT = 3,         /* precondition violated (shapes, ranges) */
+    DATTN_ERR_INTERNAL = 4,
+    DATTN_ERR_CUDA = 5,             /* CUDA runtime / launch failure; message has the CUDA string */
+    DATTN_ERR_NCCL = 6,             /* NCCL failure */
+    DATTN_ERR_CAPACITY = 7          /* page pool or block table exhausted */
+} dattn_status;
+
+typedef enum dattn_dtype { DATTN_BF16 = 0, DATTN_F32 = 1, DATTN_F64 = 2 } dattn_dtype;
+
+/* Where the q / out pointers of a decode call live. */
+typedef enum dattn_mem { DATTN_MEM_DEVICE = 0, DATTN_MEM_HOST = 1 } dattn_mem;
+
+/* kvsched.h:32 */
+const char* dattn_last_error(void);
+/* kvsched.h:34 */
+void dattn_string_free(char* s);
+/* ABI version, bumped on any signature change. */
+int dattn_abi_version(void);
+/* Number of kernel launches this thread issued since the last reset (for
+ * bench.py's gpu_launches). */
+int64_t dattn_launch_count(int reset);
+
+/* ------------------------------------------------------------------ store */
+
+/* AttentionConfig (distattention.hpp:18-29) + the paged pool geometry that
+ * replaces the reference's per-segment std::vector<double> storage
+ * (distattention.hpp:33-42) and the RManager block ledger's capacity
+ * (controlplane.hpp:126-134). */
+typedef struct dattn_store_config {
+    int head_dim;          /* >= 1; rows are zero-padded to padded_dim */
+    int num_q_heads;       /* >= 1 */
+    int num_kv_heads;      /* >= 1, divides num_q_heads */
+    double scale;          /* 0 -> 1/sqrt(head_dim) (distattention.cpp:35-37) */
+    int dtype;             /* dattn_dtype of K/V/q/out */
+    int page_tokens;       /* tokens per page = block_size_tokens (config.cpp:82 default 16) */
+    int64_t num_pages;     /* pool capacity in pages */
+    int max_seqs;          /* block-table rows */
+    int max_pages_per_seq; /* block-table columns */
+    int device;            /* CUDA device ordinal */
+} dattn_store_config;
+
+typedef struct dattn_store_info {
+    int padded_dim;        /* row length in elements (16, 32, 64, 128 or 256) */
+    int elem_bytes;
+    int record_elems;      /* partial record length = padded_dim + 4 */
+    int record_bytes;
+    int64_t free_pages;
+    int64_t used_pages;
+    int64_t pool_bytes;    /* K + V pool bytes */
+    int num_sms;
+} dattn_store_info;
+
+typedef struct dattn_store dattn_store;
+
+dattn_status dattn_store_create(const dattn_store_config* cfg, dattn_store** out);
+void dattn_store_destroy(dattn_store* s);
+dattn_status dattn_store_get_info(const dattn_store* s, dattn_store_info* out);
+/* The store's CUDA stream (cudaStream_t as void*). */
+dattn_status dattn_store_stream(const dattn_store* s, void** stream_out);
+/* Use a caller-owned stream (cudaStream_t) for all subsequent work; NULL
+ * restores the store's own stream. */
+dattn_status dattn_store_set_stream(dattn_store* s, void* stream);
+dattn_status dattn_store_synchronize(dattn_store* s);
+
+/* Launch statistics; with timing on, every K1 / K3 launch is bracketed by CUDA
+ * events on the store stream and the device time is accumulated (bench.py's
+ * roofline numerator). */
+typedef struct dattn_stats {
+    int64_t ma_launches, merge_launches;
+    int64_t ma_timed, merge_timed;
+    double ma_ms, merge_ms;     /* summed device time of timed launches */
+    int64_t last_items, last_chunks, last_plan_bytes;
+    int32_t last_chunk_tokens, ma_grid;
+} dattn_stats;
+dattn_status dattn_store_set_timing(dattn_store* s, int enable);
+dattn_status dattn_store_get_stats(dattn_store* s, int reset, dattn_stats* out);
+
+/* ------------------------------------------- sequences (block-table rows) */
+
+/* RManager::alloc_local (controlplane.cpp:38-44): allocate
+ * blocks_for_tokens(tokens) pages (perfmodel.cpp:178-182) for a new sequence
+ * and return its block-table row. Fails with DATTN_ERR_CAPACITY when the pool
+ * or the table is full (the reference returns false). */
+dattn_status dattn_seq_create(dattn_store* s, int64_t tokens, int32_t* seq_out);
+/* Grow a sequence to `tokens` (allocates pages as needed). */
+dattn_status dattn_seq_resize(dattn_store* s, int32_t seq, int64_t tokens);
+/* RManager::free_request (controlplane.cpp:55-79): release every page. */
+dattn_status dattn_seq_release(dattn_store* s, int32_t seq, int64_t* freed_pages);
+dattn_status dattn_seq_tokens(const dattn_store* s, int32_t seq, int64_t* tokens);
+/* Host copy of the block-table row (page ids). */
+dattn_status dattn_seq_block_table(const dattn_store* s, int32_t seq, int32_t* pages,
+                                   int64_t capacity, int64_t* n_pages);
+
+/* ------------------------------------------------------------- KV data */
+
+/* Write rows [tok0, tok0+n) of kv head `kv_head` of `seq` from HOST arrays
+ * k, v of n x src_row_elems elements of dtype src_dtype (src_row_elems <=
+ * padded_dim; the rest of each row is zero). Replaces building a KVSegment
+ * (distattention.hpp:33-42). Asynchronous on the store stream. */
+dattn_status dattn_kv_write(dattn_store* s, int32_t seq, int kv_head, int64_t tok0, int64_t n,
+                            const void* k, const void* v, int src_dtype, int src_row_elems);
+
+/* Read rows [tok0, tok0+n) of kv head `kv_head` of `seq` back into HOST
+ * arrays k, v of n x padded_dim elements in the store dtype (synchronous). */
+dattn_status dattn_kv_read(dattn_store* s, int32_t seq, int kv_head, int64_t tok0, int64_t n,
+                           void* k, void* v);
+
+/* K4: deterministic counter-hash fill of ALL heads of tokens [0, tokens(seq))
+ * of `seq` with the values of logical sequence `logical_seq`, logical token
+ * logical_tok0 + t (CPU twin oracle/dattn_oracle.c). */
+dattn_status dattn_kv_fill_synthetic(dattn_store* s, int32_t seq, uint64_t seed,
+                                     uint32_t logical_seq, int64_t logical_tok0,
+                                     float amp_k, float amp_v);
+
+/* Deterministic synthetic queries into a DEVICE buffer [rows][Hq][padded_dim]. */
+dattn_status dattn_q_fill_synthetic(dattn_store* s, void* q_dev, int rows, uint64_t seed,
+                                    uint32_t row0, float amp_q);
+
+/* --------------------------------------------------------- decode step */
+
+/* One rBlock: tokens [tok_begin, tok_end) of block-table row `seq`, attended
+ * by output row `out_row`. kv_head < 0: all kv heads; else only that kv head
+ * (per-kv-head segment lists, distattention.cpp:183-209). Ranges of one
+ * decode call must be sorted by out_row. An empty range contributes the
+ * identity partial (distattention.cpp:59-67). */
+typedef struct dattn_range {
+    int32_t seq;
+    int32_t out_row;
+    int32_t kv_head;
+    int32_t reserved;
+    int64_t tok_begin;
+    int64_t tok_end;
+} dattn_range;
+
+typedef struct dattn_batch {
+    int32_t num_rows;      /* output rows (requests) */
+    int32_t num_ranges;
+    const dattn_range* ranges;
+    int32_t chunk_tokens;  /* MA split granularity; 0 = auto (fills the SMs) */
+    int32_t flags;         /* DATTN_F_* */
+    double scale;          /* 0 -> store scale */
+} dattn_batch;
+
+enum {
+    DATTN_F_NO_OUTPUT = 1,    /* skip the normalised output (partials only) */
+    DATTN_F_CHECK_FINITE = 2  /* fail with DATTN_ERR_INPUT on non-finite K/V (F64 stores) */
+};
+
+/* Decode attention for every (row, q head): MA over every chunk of every
+ * range (K1), then the fused merge (K3) into
+ *   out          [num_rows][Hq][padded_dim]  normalised output (aggregate_partials,
+ *                                             distattention.cpp:150-174), and/or
+ *   row_partials [num_rows][Hq][record]      merged (m, e, ma) per row, the wire
+ *                                             partial of serialize_partial
+ *                                             (distattention.cpp:211-221),
+ * either may be NULL. q/out live in `mem` (HOST: copies are part of the call
+ * and it returns after the result is on the host; DEVICE: asynchronous on the
+ * store stream). row_partials is always a DEVICE pointer. Rows without any
+ * token produce the identity partial and a zero output. */
+dattn_status dattn_decode(dattn_store* s, const dattn_batch* b, const void* q, void* out,
+                          void* row_partials, int mem);
+
+/* K1 only: one partial record per (range, q head) -- compute_micro_attention
+ * (distattention.cpp:99-129) per rBlock, with each range processed as one
+ * chunk. partials_dev: [num_ranges][Hq][record]; heads a kv_head-specific
+ * range does not serve are written as identity. */
+dattn_status dattn_micro_attention(dattn_store* s, const dattn_batch* b, const void* q_dev,
+                                   void* partials_dev);
+
+/* K3: merge groups of partial records (combine_partials / aggregate_partials,
+ * distattention.cpp:131-174). Group g = row*heads + h merges records
+ *   index(g, c) = (row_begin ? row_begin[row] : row) * row_mul + h + c * c_stride
+ * for c in [0, row_begin ? row_begin[row+1]-row_begin[row] : n_uniform).
+ * Identity records (e == 0) are skipped; a group with one live record
+ * reproduces it bit-exactly. Writes merged records and/or normalised rows
+ * (out_norm [groups][padded_dim]) in the store dtype. All pointers DEVICE
+ * (row_begin may be NULL). */
+typedef struct dattn_merge_desc {
+    int32_t rows;
+    int32_t heads;
+    const int32_t* row_begin; /* device, rows+1 entries, or NULL */
+    int32_t n_uniform;
+    int64_t row_mul;
+    int64_t c_stride;
+} dattn_merge_desc;
+dattn_status dattn_merge_partials(dattn_store* s, const dattn_merge_desc* d, const void* recs,
+                                  void* out_recs, void* out_norm);
+
+/* ------------------------------------------------ multi-GPU (NCCL merge) */
+
+/* Sequence-sharded decode across the GPUs of one box: every
+ * rank holds its rBlocks of each request, runs K1 + local K3 into one partial
+ * per (row, q head), ncclAllGather's the packed records over NVLink and
+ * merges them with K3 -- the paper's "(o, m, l)" exchange
+ * replacing the simulated remote-partial latency of simengine.cpp:397-407. */
+#define DATTN_UNIQUE_ID_BYTES 128
+dattn_status dattn_comm_unique_id(unsigned char id[DATTN_UNIQUE_ID_BYTES]);
+dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE_ID_BYTES],
+                             int rank, int nranks);
+/* q/out as in dattn_decode; every rank passes the same num_rows. */
+dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const void* q,
+                                  void* out, int mem);
+
+/* --------------------------------------------------------- verification */
+
+/* kvs_verify_attention (kvsched.h:56-62, capi.cpp:141-155) on the GPU path:
+ * the reference's randomized equivalence trials (verify.cpp:84-186) run
+ * through the fp64 device kernels against a long-double contiguous softmax.
+ * Report format of verify.cpp:188-195. */
+dattn_status dattn_verify_attention(int trials, uint64_t seed, double tolerance,
+                                    char** report_out, int* pass_out);
+
+/* ------------------------------------------------------------- helpers */
+
+/* cudaMallocHost / cudaFreeHost for pinned staging of host q/out. */
+dattn_status dattn_host_alloc(size_t bytes, void** out);
+void dattn_host_free(void* p);
+dattn_status dattn_device_alloc(dattn_store* s, size_t bytes, void** out);
+void dattn_device_free(dattn_store* s, void* p);
+dattn_status dattn_memcpy(dattn_store* s, void* dst, const void* src, size_t bytes, int kind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DATTN_H */

@@ -1,0 +1,400 @@
+"""B200-native DistAttention decode path (Infinite-LLM, arXiv 2401.02669).
+
+Python host mirror of the C ABI in ``include/dattn.h`` (ctypes, no torch types
+in the boundary). The compute runs in ``_lib/libdattn.so`` (sm_100a kernels);
+there is no CPU fallback: importing this package without the built library
+raises ``ImportError``.
+
+Reference interface mirrored: ``kvsched::attn`` (proj/include/kvsched/
+distattention.hpp:16-95) and the C ABI conventions of proj/include/kvsched.h
+(status codes, thread-local last error). Errors map onto the reference's two
+exception kinds: ``ContractError`` (caller bug, common.hpp:11-15) and
+``InputError`` (bad data, common.hpp:17-20).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libdattn.so")
+
+BF16, F32, F64 = 0, 1, 2
+MEM_DEVICE, MEM_HOST = 0, 1
+F_NO_OUTPUT, F_CHECK_FINITE = 1, 2
+ELEM_BYTES = {BF16: 2, F32: 4, F64: 8}
+
+OK, ERR_INVALID_ARGUMENT, ERR_INPUT, ERR_CONTRACT, ERR_INTERNAL, ERR_CUDA, ERR_NCCL, ERR_CAPACITY = range(8)
+
+
+class DattnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[dattn status {status}] {msg}")
+        self.status = status
+
+
+class ContractError(DattnError):
+    """Precondition violated (kvsched::ContractError, common.hpp:11-15)."""
+
+
+class InputError(DattnError):
+    """Rejected data (kvsched::InputError, common.hpp:17-20)."""
+
+
+class CapacityError(DattnError):
+    """Page pool / block table exhausted (RManager::alloc_local returning false)."""
+
+
+class StoreConfig(ctypes.Structure):
+    _fields_ = [
+        ("head_dim", ctypes.c_int), ("num_q_heads", ctypes.c_int), ("num_kv_heads", ctypes.c_int),
+        ("scale", ctypes.c_double), ("dtype", ctypes.c_int), ("page_tokens", ctypes.c_int),
+        ("num_pages", ctypes.c_int64), ("max_seqs", ctypes.c_int),
+        ("max_pages_per_seq", ctypes.c_int), ("device", ctypes.c_int),
+    ]
+
+
+class StoreInfo(ctypes.Structure):
+    _fields_ = [
+        ("padded_dim", ctypes.c_int), ("elem_bytes", ctypes.c_int), ("record_elems", ctypes.c_int),
+        ("record_bytes", ctypes.c_int), ("free_pages", ctypes.c_int64),
+        ("used_pages", ctypes.c_int64), ("pool_bytes", ctypes.c_int64), ("num_sms", ctypes.c_int),
+    ]
+
+
+class Range(ctypes.Structure):
+    """One rBlock: tokens [tok_begin, tok_end) of a block-table row, feeding
+    output row ``out_row`` (kv_head -1: every kv head)."""
+    _fields_ = [
+        ("seq", ctypes.c_int32), ("out_row", ctypes.c_int32), ("kv_head", ctypes.c_int32),
+        ("reserved", ctypes.c_int32), ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64),
+    ]
+
+    def __init__(self, seq=0, out_row=0, tok_begin=0, tok_end=0, kv_head=-1):
+        super().__init__(seq, out_row, kv_head, 0, tok_begin, tok_end)
+
+
+class Batch(ctypes.Structure):
+    _fields_ = [
+        ("num_rows", ctypes.c_int32), ("num_ranges", ctypes.c_int32),
+        ("ranges", ctypes.POINTER(Range)), ("chunk_tokens", ctypes.c_int32),
+        ("flags", ctypes.c_int32), ("scale", ctypes.c_double),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("ma_launches", ctypes.c_int64), ("merge_launches", ctypes.c_int64),
+        ("ma_timed", ctypes.c_int64), ("merge_timed", ctypes.c_int64),
+        ("ma_ms", ctypes.c_double), ("merge_ms", ctypes.c_double),
+        ("last_items", ctypes.c_int64), ("last_chunks", ctypes.c_int64),
+        ("last_plan_bytes", ctypes.c_int64), ("last_chunk_tokens", ctypes.c_int32),
+        ("ma_grid", ctypes.c_int32),
+    ]
+
+
+class MergeDesc(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int32), ("heads", ctypes.c_int32), ("row_begin", ctypes.c_void_p),
+        ("n_uniform", ctypes.c_int32), ("row_mul", ctypes.c_int64), ("c_stride", ctypes.c_int64),
+    ]
+
+
+_FUNCS = {
+    "dattn_last_error": (ctypes.c_char_p, []),
+    "dattn_string_free": (None, [ctypes.c_void_p]),
+    "dattn_abi_version": (ctypes.c_int, []),
+    "dattn_launch_count": (ctypes.c_int64, [ctypes.c_int]),
+    "dattn_store_create": (ctypes.c_int, [ctypes.POINTER(StoreConfig), ctypes.POINTER(ctypes.c_void_p)]),
+    "dattn_store_destroy": (None, [ctypes.c_void_p]),
+    "dattn_store_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(StoreInfo)]),
+    "dattn_store_set_timing": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "dattn_store_get_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(Stats)]),
+    "dattn_store_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "dattn_store_set_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "dattn_store_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "dattn_seq_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int32)]),
+    "dattn_seq_resize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64]),
+    "dattn_seq_release": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_seq_tokens": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_seq_block_table": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                             ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_kv_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_int]),
+    "dattn_kv_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "dattn_kv_fill_synthetic": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
+                                               ctypes.c_uint32, ctypes.c_int64, ctypes.c_float,
+                                               ctypes.c_float]),
+    "dattn_q_fill_synthetic": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                              ctypes.c_uint64, ctypes.c_uint32, ctypes.c_float]),
+    "dattn_decode": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Batch), ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "dattn_micro_attention": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Batch), ctypes.c_void_p,
+                                             ctypes.c_void_p]),
+    "dattn_merge_partials": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(MergeDesc), ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p]),
+    "dattn_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "dattn_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "dattn_decode_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Batch), ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int]),
+    "dattn_verify_attention": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                              ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int)]),
+    "dattn_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "dattn_host_free": (None, [ctypes.c_void_p]),
+    "dattn_device_alloc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "dattn_device_free": (None, [ctypes.c_void_p, ctypes.c_void_p]),
+    "dattn_memcpy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                    ctypes.c_int]),
+}
+
+EXPORTED_SYMBOLS = tuple(_FUNCS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA library is not built (run __graft_entry__.build()); "
+            "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_LOCAL)
+    for name, (res, args) in _FUNCS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    s = lib.dattn_last_error()
+    return s.decode() if s else ""
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = last_error()
+    if status == ERR_CONTRACT:
+        raise ContractError(status, msg)
+    if status == ERR_INPUT:
+        raise InputError(status, msg)
+    if status == ERR_CAPACITY:
+        raise CapacityError(status, msg)
+    raise DattnError(status, msg)
+
+
+def ptr(x) -> Optional[int]:
+    """Raw address of a torch tensor / numpy array / int (None stays None)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)!r}")
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib.dattn_launch_count(1 if reset else 0))
+
+
+def blocks_for_tokens(tokens: int, block_size_tokens: int) -> int:
+    """perfmodel.cpp:178-182 -- the page-count contract of the block ledger."""
+    return (tokens + block_size_tokens - 1) // block_size_tokens
+
+
+def gqa_kv_head(query_head: int, num_q_heads: int, num_kv_heads: int) -> int:
+    """distattention.cpp:176-181 -- contiguous query-head groups."""
+    if num_q_heads < 1 or num_kv_heads < 1 or num_q_heads % num_kv_heads:
+        raise ContractError(ERR_CONTRACT, "num_q_heads must be a multiple of num_kv_heads")
+    if not 0 <= query_head < num_q_heads:
+        raise ContractError(ERR_CONTRACT, "query_head out of range")
+    return query_head // (num_q_heads // num_kv_heads)
+
+
+def effective_scale(head_dim: int, scale: float = 0.0) -> float:
+    """distattention.cpp:35-37."""
+    return scale if scale > 0.0 else 1.0 / math.sqrt(head_dim)
+
+
+def padded_dim(head_dim: int) -> int:
+    for dp in (16, 32, 64, 128, 256):
+        if head_dim <= dp:
+            return dp
+    raise ContractError(ERR_CONTRACT, "head_dim must be <= 256")
+
+
+def _batch(ranges: Sequence[Range], num_rows: int, chunk_tokens: int, flags: int, scale: float):
+    arr = (Range * max(len(ranges), 1))(*ranges)
+    b = Batch(num_rows, len(ranges), ctypes.cast(arr, ctypes.POINTER(Range)), chunk_tokens, flags, scale)
+    return b, arr
+
+
+class Store:
+    """Paged bf16/fp32/fp64 KV block store on one GPU (dattn_store)."""
+
+    def __init__(self, head_dim: int, num_q_heads: int, num_kv_heads: int, dtype: int = BF16,
+                 page_tokens: int = 16, num_pages: int = 1024, max_seqs: int = 64,
+                 max_pages_per_seq: Optional[int] = None, device: int = 0, scale: float = 0.0):
+        if max_pages_per_seq is None:
+            max_pages_per_seq = num_pages
+        cfg = StoreConfig(head_dim, num_q_heads, num_kv_heads, scale, dtype, page_tokens,
+                          num_pages, max_seqs, max_pages_per_seq, device)
+        h = ctypes.c_void_p()
+        check(lib.dattn_store_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.cfg = cfg
+        self.head_dim, self.num_q_heads, self.num_kv_heads = head_dim, num_q_heads, num_kv_heads
+        self.dtype, self.page_tokens, self.device = dtype, page_tokens, device
+        inf = self.info()
+        self.padded_dim = inf.padded_dim
+        self.record_elems = inf.record_elems
+        self.record_bytes = inf.record_bytes
+        self.elem_bytes = inf.elem_bytes
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.dattn_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> StoreInfo:
+        i = StoreInfo()
+        check(lib.dattn_store_get_info(self._h, ctypes.byref(i)))
+        return i
+
+    def set_timing(self, enable: bool):
+        check(lib.dattn_store_set_timing(self._h, 1 if enable else 0))
+
+    def stats(self, reset: bool = False) -> Stats:
+        st = Stats()
+        check(lib.dattn_store_get_stats(self._h, 1 if reset else 0, ctypes.byref(st)))
+        return st
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(lib.dattn_store_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        check(lib.dattn_store_set_stream(self._h, stream_ptr))
+
+    def synchronize(self):
+        check(lib.dattn_store_synchronize(self._h))
+
+    # --- block ledger ---
+    def seq_create(self, tokens: int) -> int:
+        out = ctypes.c_int32()
+        check(lib.dattn_seq_create(self._h, tokens, ctypes.byref(out)))
+        return out.value
+
+    def seq_resize(self, seq: int, tokens: int):
+        check(lib.dattn_seq_resize(self._h, seq, tokens))
+
+    def seq_release(self, seq: int) -> int:
+        n = ctypes.c_int64()
+        check(lib.dattn_seq_release(self._h, seq, ctypes.byref(n)))
+        return n.value
+
+    def seq_tokens(self, seq: int) -> int:
+        n = ctypes.c_int64()
+        check(lib.dattn_seq_tokens(self._h, seq, ctypes.byref(n)))
+        return n.value
+
+    def block_table(self, seq: int):
+        n = ctypes.c_int64()
+        check(lib.dattn_seq_block_table(self._h, seq, None, 0, ctypes.byref(n)))
+        arr = (ctypes.c_int32 * max(n.value, 1))()
+        check(lib.dattn_seq_block_table(self._h, seq, ctypes.cast(arr, ctypes.c_void_p), n.value,
+                                        ctypes.byref(n)))
+        return list(arr[: n.value])
+
+    # --- data ---
+    def kv_write(self, seq: int, kv_head: int, tok0: int, k, v, src_dtype: int = F64):
+        import numpy as np
+        k = np.ascontiguousarray(k)
+        v = np.ascontiguousarray(v)
+        n, d = k.shape
+        check(lib.dattn_kv_write(self._h, seq, kv_head, tok0, n, k.ctypes.data, v.ctypes.data,
+                                 src_dtype, d))
+
+    def kv_read(self, seq: int, kv_head: int, tok0: int, n: int):
+        """Rows as float64 numpy arrays [n, padded_dim] (store dtype widened)."""
+        import numpy as np
+        npdt = {BF16: np.uint16, F32: np.float32, F64: np.float64}[self.dtype]
+        k = np.zeros((n, self.padded_dim), dtype=npdt)
+        v = np.zeros((n, self.padded_dim), dtype=npdt)
+        check(lib.dattn_kv_read(self._h, seq, kv_head, tok0, n, k.ctypes.data, v.ctypes.data))
+        if self.dtype == BF16:
+            k = (k.astype(np.uint32) << 16).view(np.float32)
+            v = (v.astype(np.uint32) << 16).view(np.float32)
+        return k.astype(np.float64), v.astype(np.float64)
+
+    def fill_synthetic(self, seq: int, seed: int, logical_seq: int, logical_tok0: int = 0,
+                       amp_k: float = 1.0, amp_v: float = 2.0):
+        check(lib.dattn_kv_fill_synthetic(self._h, seq, seed, logical_seq, logical_tok0, amp_k, amp_v))
+
+    def q_fill_synthetic(self, q_dev, rows: int, seed: int, row0: int = 0, amp_q: float = 1.0):
+        check(lib.dattn_q_fill_synthetic(self._h, ptr(q_dev), rows, seed, row0, amp_q))
+
+    # --- compute ---
+    def decode(self, ranges: Sequence[Range], num_rows: int, q, out, row_partials=None,
+               mem: int = MEM_DEVICE, chunk_tokens: int = 0, flags: int = 0, scale: float = 0.0):
+        b, keep = _batch(ranges, num_rows, chunk_tokens, flags, scale)
+        check(lib.dattn_decode(self._h, ctypes.byref(b), ptr(q), ptr(out), ptr(row_partials), mem))
+
+    def micro_attention(self, ranges: Sequence[Range], num_rows: int, q_dev, partials_dev,
+                        flags: int = 0, scale: float = 0.0):
+        b, keep = _batch(ranges, num_rows, 0, flags, scale)
+        check(lib.dattn_micro_attention(self._h, ctypes.byref(b), ptr(q_dev), ptr(partials_dev)))
+
+    def merge(self, recs, rows: int, heads: int, n_uniform: int, row_mul: int, c_stride: int,
+              out_recs=None, out_norm=None, row_begin=None):
+        d = MergeDesc(rows, heads, ptr(row_begin), n_uniform, row_mul, c_stride)
+        check(lib.dattn_merge_partials(self._h, ctypes.byref(d), ptr(recs), ptr(out_recs), ptr(out_norm)))
+
+    # --- multi-GPU ---
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int):
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        check(lib.dattn_comm_init(self._h, buf, rank, nranks))
+
+    def decode_sharded(self, ranges: Sequence[Range], num_rows: int, q, out, mem: int = MEM_DEVICE,
+                       chunk_tokens: int = 0, scale: float = 0.0):
+        b, keep = _batch(ranges, num_rows, chunk_tokens, 0, scale)
+        check(lib.dattn_decode_sharded(self._h, ctypes.byref(b), ptr(q), ptr(out), mem))
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib.dattn_comm_unique_id(buf))
+    return buf.raw
+
+
+def verify_attention(trials: int, seed: int, tolerance: float):
+    """kvs_verify_attention (kvsched.h:56-62) on the GPU path. Returns (report, pass)."""
+    rep = ctypes.c_void_p()
+    ok = ctypes.c_int(-1)
+    check(lib.dattn_verify_attention(trials, seed, tolerance, ctypes.byref(rep), ctypes.byref(ok)))
+    text = ctypes.string_at(rep.value).decode()
+    lib.dattn_string_free(rep)
+    return text, bool(ok.value)
+
+
+from .sharding import plan_rank_ranges, placement_from_moves, RankRange  # noqa: E402,F401

@@ -1,0 +1,907 @@
+// dattn_engine.cpp -- host engine behind the C ABI (include/dattn.h): the
+// paged KV store and its page ledger, the decode planner (ranges -> MA work
+// items -> partial records), kernel launches, and the NCCL partial exchange.
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dattn.h"
+#include "dattn_engine.h"
+#include "dattn_internal.h"
+
+using namespace dattn;
+
+namespace dattn {
+
+thread_local std::string g_last_error = "";
+thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+Error::Error(dattn_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(DATTN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Error(DATTN_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+void count_launch(int n) { g_launches += n; }
+
+void DevBuf::ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cuda_check(cudaMalloc(&p, want), "cudaMalloc");
+    cap = want;
+}
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+void HostBuf::ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cuda_check(cudaMallocHost(&p, want), "cudaMallocHost");
+    cap = want;
+}
+HostBuf::~HostBuf() {
+    if (p) cudaFreeHost(p);
+}
+
+int padded_dim_for(int head_dim) {
+    for (int dp : {16, 32, 64, 128, 256})
+        if (head_dim <= dp) return dp;
+    return -1;
+}
+
+int elem_bytes_for(int dtype) { return dtype == kBF16 ? 2 : (dtype == kF32 ? 4 : 8); }
+
+}  // namespace dattn
+
+// ------------------------------------------------------------------ store
+
+dattn_store::~dattn_store() {
+    if (comm) ncclCommDestroy(comm);
+    for (auto* v : {&ma_events, &merge_events})
+        for (auto& pr : *v) {
+            cudaEventDestroy(pr[0]);
+            cudaEventDestroy(pr[1]);
+        }
+    if (kpool) cudaFree(kpool);
+    if (vpool) cudaFree(vpool);
+    if (d_bt) cudaFree(d_bt);
+    if (d_counter) cudaFree(d_counter);
+    if (d_flag) cudaFree(d_flag);
+    if (meta_ev) cudaEventDestroy(meta_ev);
+    if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+void dattn_store::activate() const { cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice"); }
+
+static void validate_config(const dattn_store_config& c) {
+    if (c.head_dim < 1 || c.head_dim > 256)
+        throw Error(DATTN_ERR_CONTRACT, "head_dim must be in [1, 256]");
+    if (c.num_q_heads < 1 || c.num_kv_heads < 1)
+        throw Error(DATTN_ERR_CONTRACT, "head counts must be >= 1");
+    if (c.num_q_heads % c.num_kv_heads != 0)
+        throw Error(DATTN_ERR_CONTRACT, "num_q_heads must be a multiple of num_kv_heads");
+    if (!std::isfinite(c.scale) || c.scale < 0.0)
+        throw Error(DATTN_ERR_CONTRACT, "scale must be finite and >= 0");
+    if (c.dtype < 0 || c.dtype > 2) throw Error(DATTN_ERR_INVALID_ARGUMENT, "unknown dtype");
+    if (c.page_tokens < 1) throw Error(DATTN_ERR_CONTRACT, "page_tokens must be >= 1");
+    if (c.num_pages < 1 || c.num_pages > (int64_t(1) << 31) - 1)
+        throw Error(DATTN_ERR_CONTRACT, "num_pages out of range");
+    if (c.max_seqs < 1 || c.max_pages_per_seq < 1)
+        throw Error(DATTN_ERR_CONTRACT, "block-table shape must be >= 1");
+    const int g = c.num_q_heads / c.num_kv_heads;
+    if (g > (c.dtype == kF64 ? 8 : 16))
+        throw Error(DATTN_ERR_CONTRACT, "query group size too large for the MA kernel");
+}
+
+void dattn_store::init(const dattn_store_config& c) {
+    validate_config(c);
+    cfg = c;
+    dp = padded_dim_for(c.head_dim);
+    esz = elem_bytes_for(c.dtype);
+    acc_sz = c.dtype == kF64 ? 8 : 4;
+    rec_elems = dp + 4;
+    group = c.num_q_heads / c.num_kv_heads;
+    activate();
+    cuda_check(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream = own_stream;
+    cuda_check(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming), "cudaEventCreate");
+    int dev = c.device;
+    cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev),
+               "cudaDeviceGetAttribute");
+    page_elems = static_cast<int64_t>(c.num_kv_heads) * c.page_tokens * dp;
+    const size_t pool = static_cast<size_t>(c.num_pages) * page_elems * esz;
+    cuda_check(cudaMalloc(&kpool, pool), "cudaMalloc(K pool)");
+    cuda_check(cudaMalloc(&vpool, pool), "cudaMalloc(V pool)");
+    cuda_check(cudaMemsetAsync(kpool, 0, pool, stream), "cudaMemset");
+    cuda_check(cudaMemsetAsync(vpool, 0, pool, stream), "cudaMemset");
+    const size_t bt = static_cast<size_t>(c.max_seqs) * c.max_pages_per_seq * sizeof(int32_t);
+    cuda_check(cudaMalloc(&d_bt, bt), "cudaMalloc(block tables)");
+    cuda_check(cudaMemsetAsync(d_bt, 0, bt, stream), "cudaMemset");
+    cuda_check(cudaMalloc(&d_counter, 64), "cudaMalloc");
+    cuda_check(cudaMalloc(&d_flag, 64), "cudaMalloc");
+    h_bt.assign(static_cast<size_t>(c.max_seqs) * c.max_pages_per_seq, 0);
+    seq_tokens.assign(c.max_seqs, 0);
+    seq_pages.assign(c.max_seqs, 0);
+    seq_live.assign(c.max_seqs, 0);
+    free_pages.reserve(c.num_pages);
+    for (int64_t i = c.num_pages - 1; i >= 0; --i) free_pages.push_back(static_cast<int32_t>(i));
+    for (int i = c.max_seqs - 1; i >= 0; --i) free_seqs.push_back(i);
+
+    // MA launch geometry: the deepest ring that still fits the target CTAs/SM.
+    const char* env_ctas = std::getenv("DATTN_MA_CTAS");
+    const char* env_stages = std::getenv("DATTN_MA_STAGES");
+    int want_ctas = (c.dtype == kF64 || group > 8) ? 1 : 2;
+    if (env_ctas) want_ctas = std::max(1, std::atoi(env_ctas));
+    const size_t sm_total = 233472;  // 228 KB per SM
+    int stages = 2;
+    for (int s = 2; s <= 12; ++s) {
+        const size_t need = ma_smem_bytes(c.dtype, dp, group, s);
+        if ((need + 1024) * want_ctas <= sm_total && need <= 232448) stages = s;
+    }
+    if (env_stages) stages = std::max(2, std::atoi(env_stages));
+    ma_stages = stages;
+    ma_smem = ma_smem_bytes(c.dtype, dp, group, stages);
+    cuda_check(ma_configure(c.dtype, dp, group, ma_smem), "cudaFuncSetAttribute(MA)");
+    int occ = 0;
+    cuda_check(ma_occupancy(c.dtype, dp, group, ma_smem, &occ), "occupancy(MA)");
+    ma_ctas_per_sm = std::max(1, occ);
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+}
+
+void dattn_store::upload_bt_row(int32_t seq) {
+    const size_t off = static_cast<size_t>(seq) * cfg.max_pages_per_seq;
+    const int32_t n = seq_pages[seq];
+    if (n == 0) return;
+    cuda_check(cudaMemcpyAsync(d_bt + off, h_bt.data() + off, sizeof(int32_t) * n,
+                               cudaMemcpyHostToDevice, stream),
+               "cudaMemcpyAsync(block table)");
+}
+
+void dattn_store::check_seq(int32_t seq) const {
+    if (seq < 0 || seq >= cfg.max_seqs || !seq_live[seq])
+        throw Error(DATTN_ERR_CONTRACT, "unknown sequence id " + std::to_string(seq));
+}
+
+void dattn_store::grow(int32_t seq, int64_t tokens) {
+    const int64_t need = (tokens + cfg.page_tokens - 1) / cfg.page_tokens;  // blocks_for_tokens
+    if (need > cfg.max_pages_per_seq)
+        throw Error(DATTN_ERR_CAPACITY, "sequence exceeds max_pages_per_seq");
+    const int64_t add = need - seq_pages[seq];
+    if (add > static_cast<int64_t>(free_pages.size()))
+        throw Error(DATTN_ERR_CAPACITY, "page pool exhausted");
+    const size_t off = static_cast<size_t>(seq) * cfg.max_pages_per_seq;
+    for (int64_t i = 0; i < add; ++i) {
+        h_bt[off + seq_pages[seq] + i] = free_pages.back();
+        free_pages.pop_back();
+    }
+    if (add > 0) {
+        seq_pages[seq] = static_cast<int32_t>(need);
+        used_pages += add;
+        upload_bt_row(seq);
+    }
+    seq_tokens[seq] = std::max(seq_tokens[seq], tokens);
+}
+
+// ----------------------------------------------------------------- planner
+
+void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl) const {
+    if (b.num_rows < 0 || b.num_ranges < 0)
+        throw Error(DATTN_ERR_INVALID_ARGUMENT, "negative row/range count");
+    if (b.num_ranges > 0 && !b.ranges)
+        throw Error(DATTN_ERR_INVALID_ARGUMENT, "ranges is null");
+    const int nr = b.num_ranges;
+    int64_t work = 0, max_len = 0;
+    int prev_row = -1;
+    for (int i = 0; i < nr; ++i) {
+        const dattn_range& r = b.ranges[i];
+        check_seq(r.seq);
+        if (r.out_row < 0 || r.out_row >= b.num_rows)
+            throw Error(DATTN_ERR_CONTRACT, "range out_row out of bounds");
+        if (r.out_row < prev_row) throw Error(DATTN_ERR_CONTRACT, "ranges must be sorted by out_row");
+        prev_row = r.out_row;
+        if (r.kv_head < -1 || r.kv_head >= cfg.num_kv_heads)
+            throw Error(DATTN_ERR_CONTRACT, "range kv_head out of bounds");
+        if (r.tok_begin < 0 || r.tok_begin > r.tok_end || r.tok_end > seq_tokens[r.seq])
+            throw Error(DATTN_ERR_CONTRACT, "range tokens outside the sequence");
+        if (r.tok_end > INT32_MAX) throw Error(DATTN_ERR_CONTRACT, "range too long");
+        const int64_t len = r.tok_end - r.tok_begin;
+        work += len * (r.kv_head < 0 ? cfg.num_kv_heads : 1);
+        max_len = std::max(max_len, len);
+    }
+    int64_t C;
+    if (one_chunk_per_range) {
+        C = std::max<int64_t>(max_len, 1);
+    } else if (b.chunk_tokens > 0) {
+        C = b.chunk_tokens;
+    } else {
+        const int64_t target = static_cast<int64_t>(num_sms) * ma_ctas_per_sm * 12;
+        int64_t c = std::max<int64_t>(work / std::max<int64_t>(target, 1), 1);
+        int64_t p2 = 1;
+        while (p2 * 2 <= c) p2 *= 2;
+        const int64_t lo = std::max<int64_t>(ma_stage_tokens(cfg.dtype, dp), 64);
+        C = std::min<int64_t>(std::max<int64_t>(p2, lo), 2048);
+        if (C % cfg.page_tokens) C = (C / cfg.page_tokens + 1) * cfg.page_tokens;
+    }
+    if (C > INT32_MAX) throw Error(DATTN_ERR_CONTRACT, "chunk too long");
+    pl.chunk_tokens = static_cast<int32_t>(C);
+
+    // layout of the metadata buffer (int32 words)
+    pl.off_ranges = 0;
+    pl.off_item = pl.off_ranges + 8 * nr;
+    pl.off_chunk = pl.off_item + nr + 1;
+    pl.off_rowchunk = pl.off_chunk + nr + 1;
+    pl.off_kvh = pl.off_rowchunk + b.num_rows + 1;
+    // first pass: counts
+    pl.words.assign(pl.off_kvh, 0);
+    int64_t items = 0, chunks = 0;
+    std::vector<int32_t> row_chunks(b.num_rows, 0);
+    for (int i = 0; i < nr; ++i) {
+        const dattn_range& r = b.ranges[i];
+        const int64_t len = r.tok_end - r.tok_begin;
+        const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
+        const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
+        RangeDev rd{r.seq, r.out_row, r.kv_head, static_cast<int32_t>(r.tok_begin),
+                    static_cast<int32_t>(r.tok_end), {0, 0, 0}};
+        std::memcpy(&pl.words[pl.off_ranges + 8 * i], &rd, sizeof(rd));
+        pl.words[pl.off_item + i] = static_cast<int32_t>(items);
+        pl.words[pl.off_chunk + i] = one_chunk_per_range ? i : static_cast<int32_t>(chunks);
+        items += nch * nh;
+        chunks += nch;
+        row_chunks[r.out_row] += static_cast<int32_t>(nch);
+        if (items > INT32_MAX) throw Error(DATTN_ERR_CONTRACT, "too many work items");
+    }
+    pl.words[pl.off_item + nr] = static_cast<int32_t>(items);
+    pl.words[pl.off_chunk + nr] = one_chunk_per_range ? nr : static_cast<int32_t>(chunks);
+    int32_t acc = 0;
+    for (int rrow = 0; rrow < b.num_rows; ++rrow) {
+        pl.words[pl.off_rowchunk + rrow] = acc;
+        acc += row_chunks[rrow];
+    }
+    pl.words[pl.off_rowchunk + b.num_rows] = acc;
+    pl.words.resize(pl.off_kvh + static_cast<size_t>(chunks));
+    bool any_kvh = false;
+    int64_t c = 0;
+    for (int i = 0; i < nr; ++i) {
+        const dattn_range& r = b.ranges[i];
+        const int64_t len = r.tok_end - r.tok_begin;
+        const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
+        for (int64_t k = 0; k < nch; ++k) pl.words[pl.off_kvh + c++] = r.kv_head;
+        any_kvh |= r.kv_head >= 0;
+    }
+    pl.any_kvh = any_kvh;
+    pl.nitems = static_cast<int32_t>(items);
+    pl.nchunks = static_cast<int32_t>(one_chunk_per_range ? nr : chunks);
+    pl.nranges = nr;
+    pl.nrows = b.num_rows;
+}
+
+void dattn_store::upload_plan(const Plan& pl) {
+    const size_t bytes = pl.words.size() * sizeof(int32_t);
+    stats.last_plan_bytes = static_cast<int64_t>(bytes);
+    // the previous call's H2D copy must have consumed the pinned staging
+    cuda_check(cudaEventSynchronize(meta_ev), "cudaEventSynchronize");
+    h_meta.ensure(bytes);
+    d_meta.ensure(bytes);
+    std::memcpy(h_meta.p, pl.words.data(), bytes);
+    cuda_check(cudaMemcpyAsync(d_meta.p, h_meta.p, bytes, cudaMemcpyHostToDevice, stream),
+               "cudaMemcpyAsync(plan)");
+    cuda_check(cudaEventRecord(meta_ev, stream), "cudaEventRecord");
+}
+
+void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double scale,
+                         bool check_finite) {
+    if (pl.nitems == 0) return;
+    const int32_t* w = static_cast<const int32_t*>(d_meta.p);
+    MAParams p{};
+    p.k_pool = kpool;
+    p.v_pool = vpool;
+    p.block_tables = d_bt;
+    p.bt_stride = cfg.max_pages_per_seq;
+    p.page_tokens = cfg.page_tokens;
+    p.num_kv_heads = cfg.num_kv_heads;
+    p.num_q_heads = cfg.num_q_heads;
+    p.group = group;
+    p.q = q_dev;
+    p.ranges = reinterpret_cast<const RangeDev*>(w + pl.off_ranges);
+    p.item_prefix = w + pl.off_item;
+    p.chunk_prefix = w + pl.off_chunk;
+    p.nranges = pl.nranges;
+    p.nitems = pl.nitems;
+    p.chunk_tokens = pl.chunk_tokens;
+    const double s = scale > 0.0 ? scale : effective_scale();
+    p.scale_log2 = s * 1.4426950408889634074;
+    p.records = recs;
+    p.work_counter = d_counter;
+    p.nonfinite_flag = check_finite ? d_flag : nullptr;
+    p.stages = ma_stages;
+    cuda_check(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
+    const int grid = std::max(1, std::min(pl.nitems, num_sms * ma_ctas_per_sm));
+    cudaEvent_t* ev = timing ? timer_pair(0) : nullptr;
+    if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
+    cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
+    if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+    count_launch(1);
+    stats.ma_launches++;
+    stats.last_items = pl.nitems;
+    stats.last_chunks = pl.nchunks;
+    stats.last_chunk_tokens = pl.chunk_tokens;
+    stats.ma_grid = grid;
+}
+
+double dattn_store::effective_scale() const {
+    return cfg.scale > 0.0 ? cfg.scale : 1.0 / std::sqrt(static_cast<double>(cfg.head_dim));
+}
+
+void dattn_store::run_merge(const MergeParams& mp) {
+    cudaEvent_t* ev = timing ? timer_pair(1) : nullptr;
+    if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
+    cuda_check(launch_merge(cfg.dtype, dp, mp, stream), "launch(merge)");
+    if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+    count_launch(1);
+    stats.merge_launches++;
+}
+
+// Event pairs around every MA (kind 0) / merge (kind 1) launch while timing
+// is on; summed by dattn_store_get_stats.
+cudaEvent_t* dattn_store::timer_pair(int kind) {
+    auto& v = kind == 0 ? ma_events : merge_events;
+    auto& used = kind == 0 ? ma_events_used : merge_events_used;
+    if (used == v.size()) {
+        std::array<cudaEvent_t, 2> pr{};
+        cuda_check(cudaEventCreate(&pr[0]), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&pr[1]), "cudaEventCreate");
+        v.push_back(pr);
+    }
+    return v[used++].data();
+}
+
+void dattn_store::collect_timing() {
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    for (int kind = 0; kind < 2; ++kind) {
+        auto& v = kind == 0 ? ma_events : merge_events;
+        auto& used = kind == 0 ? ma_events_used : merge_events_used;
+        double total = 0.0;
+        for (size_t i = 0; i < used; ++i) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, v[i][0], v[i][1]), "cudaEventElapsedTime");
+            total += ms;
+        }
+        if (kind == 0) { stats.ma_ms += total; stats.ma_timed += used; }
+        else { stats.merge_ms += total; stats.merge_timed += used; }
+        used = 0;
+    }
+}
+
+void dattn_store::local_merge(const Plan& pl, const void* recs, void* out_recs, void* out_norm) {
+    const int32_t* w = static_cast<const int32_t*>(d_meta.p);
+    MergeParams mp{};
+    mp.recs = recs;
+    mp.rows = pl.nrows;
+    mp.heads = cfg.num_q_heads;
+    mp.row_begin = w + pl.off_rowchunk;
+    mp.row_mul = cfg.num_q_heads;
+    mp.c_stride = cfg.num_q_heads;
+    mp.chunk_kvh = pl.any_kvh ? w + pl.off_kvh : nullptr;
+    mp.group = group;
+    mp.out_recs = out_recs;
+    mp.out_norm = out_norm;
+    run_merge(mp);
+}
+
+size_t dattn_store::q_bytes(int rows) const {
+    return static_cast<size_t>(rows) * cfg.num_q_heads * dp * esz;
+}
+size_t dattn_store::rec_bytes() const { return static_cast<size_t>(rec_elems) * acc_sz; }
+
+void dattn_store::check_flag() {
+    int32_t flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, stream),
+               "cudaMemcpyAsync(flag)");
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    if (flag) throw Error(DATTN_ERR_INPUT, "segment contains non-finite values");
+}
+
+void dattn_store::decode(const dattn_batch& b, const void* q, void* out, void* row_partials,
+                         int mem) {
+    activate();
+    Plan& pl = scratch_plan;
+    plan(b, false, pl);
+    upload_plan(pl);
+    const bool want_out = out && !(b.flags & DATTN_F_NO_OUTPUT);
+    const void* q_dev = q;
+    if (mem == DATTN_MEM_HOST) {
+        qbuf.ensure(q_bytes(b.num_rows));
+        cuda_check(cudaMemcpyAsync(qbuf.p, q, q_bytes(b.num_rows), cudaMemcpyHostToDevice, stream),
+                   "cudaMemcpyAsync(q)");
+        q_dev = qbuf.p;
+    }
+    const bool check = (b.flags & DATTN_F_CHECK_FINITE) != 0;
+    if (check) cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
+    recs.ensure(static_cast<size_t>(std::max(pl.nchunks, 1)) * cfg.num_q_heads * rec_bytes());
+    run_ma(pl, q_dev, recs.p, b.scale, check);
+    void* out_dev = out;
+    if (want_out && mem == DATTN_MEM_HOST) {
+        obuf.ensure(q_bytes(b.num_rows));
+        out_dev = obuf.p;
+    }
+    local_merge(pl, recs.p, row_partials, want_out ? out_dev : nullptr);
+    if (mem == DATTN_MEM_HOST) {
+        if (want_out)
+            cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost,
+                                       stream),
+                       "cudaMemcpyAsync(out)");
+        cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    }
+    if (check) check_flag();
+}
+
+void dattn_store::micro_attention(const dattn_batch& b, const void* q_dev, void* partials) {
+    activate();
+    Plan& pl = scratch_plan;
+    plan(b, true, pl);
+    upload_plan(pl);
+    const bool check = (b.flags & DATTN_F_CHECK_FINITE) != 0;
+    if (check) cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
+    const int64_t n = static_cast<int64_t>(b.num_ranges) * cfg.num_q_heads;
+    if (n > 0) {
+        cuda_check(launch_identity_records(cfg.dtype, dp, partials, n, stream), "launch(identity)");
+        count_launch(1);
+    }
+    run_ma(pl, q_dev, partials, b.scale, check);
+    if (check) check_flag();
+}
+
+void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out, int mem) {
+    if (!comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
+    activate();
+    Plan& pl = scratch_plan;
+    plan(b, false, pl);
+    upload_plan(pl);
+    const void* q_dev = q;
+    if (mem == DATTN_MEM_HOST) {
+        qbuf.ensure(q_bytes(b.num_rows));
+        cuda_check(cudaMemcpyAsync(qbuf.p, q, q_bytes(b.num_rows), cudaMemcpyHostToDevice, stream),
+                   "cudaMemcpyAsync(q)");
+        q_dev = qbuf.p;
+    }
+    recs.ensure(static_cast<size_t>(std::max(pl.nchunks, 1)) * cfg.num_q_heads * rec_bytes());
+    run_ma(pl, q_dev, recs.p, b.scale, false);
+    const size_t row_recs = static_cast<size_t>(b.num_rows) * cfg.num_q_heads;
+    rowrecs.ensure(std::max<size_t>(row_recs, 1) * rec_bytes());
+    local_merge(pl, recs.p, rowrecs.p, nullptr);
+    gathered.ensure(std::max<size_t>(row_recs, 1) * rec_bytes() * nranks);
+    nccl_check(ncclAllGather(rowrecs.p, gathered.p, row_recs * rec_elems,
+                             cfg.dtype == kF64 ? ncclDouble : ncclFloat32, comm, stream),
+               "ncclAllGather(partials)");
+    MergeParams mp{};
+    mp.recs = gathered.p;
+    mp.rows = b.num_rows;
+    mp.heads = cfg.num_q_heads;
+    mp.row_begin = nullptr;
+    mp.n_uniform = nranks;
+    mp.row_mul = cfg.num_q_heads;
+    mp.c_stride = static_cast<int64_t>(row_recs);
+    mp.group = group;
+    void* out_dev = out;
+    if (mem == DATTN_MEM_HOST) {
+        obuf.ensure(q_bytes(b.num_rows));
+        out_dev = obuf.p;
+    }
+    mp.out_norm = out_dev;
+    run_merge(mp);
+    if (mem == DATTN_MEM_HOST) {
+        cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost, stream),
+                   "cudaMemcpyAsync(out)");
+        cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    }
+}
+
+// ------------------------------------------------------------------ C ABI
+
+template <class F>
+static dattn_status guarded(F&& f) {
+    try {
+        f();
+        return DATTN_OK;
+    } catch (const Error& e) {
+        set_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_error("out of host memory");
+        return DATTN_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return DATTN_ERR_INTERNAL;
+    }
+}
+
+#define REQUIRE_ARG(cond, msg) \
+    do { if (!(cond)) throw Error(DATTN_ERR_INVALID_ARGUMENT, msg); } while (0)
+
+extern "C" {
+
+const char* dattn_last_error(void) { return g_last_error.c_str(); }
+void dattn_string_free(char* s) { std::free(s); }
+int dattn_abi_version(void) { return 1; }
+int64_t dattn_launch_count(int reset) {
+    const int64_t n = g_launches;
+    if (reset) g_launches = 0;
+    return n;
+}
+
+dattn_status dattn_store_create(const dattn_store_config* cfg, dattn_store** out) {
+    return guarded([&] {
+        REQUIRE_ARG(cfg && out, "null argument");
+        auto* s = new dattn_store();
+        try {
+            s->init(*cfg);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+void dattn_store_destroy(dattn_store* s) {
+    if (!s) return;
+    cudaSetDevice(s->cfg.device);
+    cudaStreamSynchronize(s->stream);
+    delete s;
+}
+
+dattn_status dattn_store_get_info(const dattn_store* s, dattn_store_info* out) {
+    return guarded([&] {
+        REQUIRE_ARG(s && out, "null argument");
+        out->padded_dim = s->dp;
+        out->elem_bytes = s->esz;
+        out->record_elems = s->rec_elems;
+        out->record_bytes = static_cast<int>(s->rec_bytes());
+        out->free_pages = static_cast<int64_t>(s->free_pages.size());
+        out->used_pages = s->used_pages;
+        out->pool_bytes = 2 * s->cfg.num_pages * s->page_elems * s->esz;
+        out->num_sms = s->num_sms;
+    });
+}
+
+dattn_status dattn_store_set_timing(dattn_store* s, int enable) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->activate();
+        if (s->timing) s->collect_timing();
+        s->timing = enable != 0;
+    });
+}
+
+dattn_status dattn_store_get_stats(dattn_store* s, int reset, dattn_stats* out) {
+    return guarded([&] {
+        REQUIRE_ARG(s && out, "null argument");
+        s->activate();
+        if (s->timing) s->collect_timing();
+        *out = s->stats;
+        if (reset) {
+            const dattn_stats keep = s->stats;
+            s->stats = dattn_stats{};
+            s->stats.ma_grid = keep.ma_grid;
+        }
+    });
+}
+
+dattn_status dattn_store_stream(const dattn_store* s, void** stream_out) {
+    return guarded([&] {
+        REQUIRE_ARG(s && stream_out, "null argument");
+        *stream_out = s->stream;
+    });
+}
+
+dattn_status dattn_store_set_stream(dattn_store* s, void* stream) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->activate();
+        // order the switch after all work already queued on the old stream
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+        s->stream = stream ? static_cast<cudaStream_t>(stream) : s->own_stream;
+    });
+}
+
+dattn_status dattn_store_synchronize(dattn_store* s) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->activate();
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    });
+}
+
+dattn_status dattn_seq_create(dattn_store* s, int64_t tokens, int32_t* seq_out) {
+    return guarded([&] {
+        REQUIRE_ARG(s && seq_out, "null argument");
+        if (tokens < 0) throw Error(DATTN_ERR_CONTRACT, "token count must be >= 0");
+        if (s->free_seqs.empty()) throw Error(DATTN_ERR_CAPACITY, "block table full");
+        s->activate();
+        const int32_t id = s->free_seqs.back();
+        const int64_t need = (tokens + s->cfg.page_tokens - 1) / s->cfg.page_tokens;
+        if (need > s->cfg.max_pages_per_seq)
+            throw Error(DATTN_ERR_CAPACITY, "sequence exceeds max_pages_per_seq");
+        if (need > static_cast<int64_t>(s->free_pages.size()))
+            throw Error(DATTN_ERR_CAPACITY, "page pool exhausted");
+        s->free_seqs.pop_back();
+        s->seq_live[id] = 1;
+        s->seq_pages[id] = 0;
+        s->seq_tokens[id] = 0;
+        s->grow(id, tokens);
+        *seq_out = id;
+    });
+}
+
+dattn_status dattn_seq_resize(dattn_store* s, int32_t seq, int64_t tokens) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->check_seq(seq);
+        if (tokens < s->seq_tokens[seq]) throw Error(DATTN_ERR_CONTRACT, "sequences only grow");
+        s->activate();
+        s->grow(seq, tokens);
+    });
+}
+
+dattn_status dattn_seq_release(dattn_store* s, int32_t seq, int64_t* freed_pages) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->check_seq(seq);
+        const size_t off = static_cast<size_t>(seq) * s->cfg.max_pages_per_seq;
+        const int32_t n = s->seq_pages[seq];
+        for (int32_t i = n - 1; i >= 0; --i) s->free_pages.push_back(s->h_bt[off + i]);
+        s->used_pages -= n;
+        s->seq_pages[seq] = 0;
+        s->seq_tokens[seq] = 0;
+        s->seq_live[seq] = 0;
+        s->free_seqs.push_back(seq);
+        if (freed_pages) *freed_pages = n;
+    });
+}
+
+dattn_status dattn_seq_tokens(const dattn_store* s, int32_t seq, int64_t* tokens) {
+    return guarded([&] {
+        REQUIRE_ARG(s && tokens, "null argument");
+        s->check_seq(seq);
+        *tokens = s->seq_tokens[seq];
+    });
+}
+
+dattn_status dattn_seq_block_table(const dattn_store* s, int32_t seq, int32_t* pages,
+                                   int64_t capacity, int64_t* n_pages) {
+    return guarded([&] {
+        REQUIRE_ARG(s && n_pages, "null argument");
+        s->check_seq(seq);
+        const int32_t n = s->seq_pages[seq];
+        if (pages) {
+            if (capacity < n) throw Error(DATTN_ERR_INVALID_ARGUMENT, "capacity too small");
+            std::memcpy(pages, s->h_bt.data() + static_cast<size_t>(seq) * s->cfg.max_pages_per_seq,
+                        sizeof(int32_t) * n);
+        }
+        *n_pages = n;
+    });
+}
+
+dattn_status dattn_kv_write(dattn_store* s, int32_t seq, int kv_head, int64_t tok0, int64_t n,
+                            const void* k, const void* v, int src_dtype, int src_row_elems) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->check_seq(seq);
+        if (n == 0) return;
+        REQUIRE_ARG(k && v, "null data");
+        if (kv_head < 0 || kv_head >= s->cfg.num_kv_heads)
+            throw Error(DATTN_ERR_CONTRACT, "kv_head out of bounds");
+        if (tok0 < 0 || n < 0 || tok0 + n > s->seq_tokens[seq])
+            throw Error(DATTN_ERR_CONTRACT, "rows outside the sequence");
+        if (src_row_elems < 1 || src_row_elems > s->dp)
+            throw Error(DATTN_ERR_CONTRACT, "row length exceeds the padded head dim");
+        if (src_dtype < 0 || src_dtype > 2) throw Error(DATTN_ERR_INVALID_ARGUMENT, "unknown dtype");
+        s->activate();
+        s->write_rows(seq, kv_head, tok0, n, k, v, src_dtype, src_row_elems);
+    });
+}
+
+dattn_status dattn_kv_read(dattn_store* s, int32_t seq, int kv_head, int64_t tok0, int64_t n,
+                           void* k, void* v) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->check_seq(seq);
+        if (n == 0) return;
+        REQUIRE_ARG(k && v, "null data");
+        if (kv_head < 0 || kv_head >= s->cfg.num_kv_heads)
+            throw Error(DATTN_ERR_CONTRACT, "kv_head out of bounds");
+        if (tok0 < 0 || n < 0 || tok0 + n > s->seq_tokens[seq])
+            throw Error(DATTN_ERR_CONTRACT, "rows outside the sequence");
+        s->activate();
+        const size_t bytes = static_cast<size_t>(n) * s->dp * s->esz;
+        DevBuf tmp;
+        tmp.ensure(2 * bytes);
+        ScatterParams p{};
+        p.k_pool = s->kpool;
+        p.v_pool = s->vpool;
+        p.k_rows = tmp.p;
+        p.v_rows = static_cast<uint8_t*>(tmp.p) + bytes;
+        p.block_row = s->d_bt + static_cast<size_t>(seq) * s->cfg.max_pages_per_seq;
+        p.page_tokens = s->cfg.page_tokens;
+        p.num_kv_heads = s->cfg.num_kv_heads;
+        p.kv_head = kv_head;
+        p.tok0 = tok0;
+        p.n = n;
+        cuda_check(launch_gather(s->cfg.dtype, s->dp, p, s->stream), "launch(gather)");
+        count_launch(1);
+        cuda_check(cudaMemcpyAsync(k, tmp.p, bytes, cudaMemcpyDeviceToHost, s->stream), "cudaMemcpyAsync");
+        cuda_check(cudaMemcpyAsync(v, p.v_rows, bytes, cudaMemcpyDeviceToHost, s->stream), "cudaMemcpyAsync");
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    });
+}
+
+dattn_status dattn_kv_fill_synthetic(dattn_store* s, int32_t seq, uint64_t seed,
+                                     uint32_t logical_seq, int64_t logical_tok0, float amp_k,
+                                     float amp_v) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        s->check_seq(seq);
+        s->activate();
+        FillParams p{};
+        p.k_pool = s->kpool;
+        p.v_pool = s->vpool;
+        p.block_row = s->d_bt + static_cast<size_t>(seq) * s->cfg.max_pages_per_seq;
+        p.page_tokens = s->cfg.page_tokens;
+        p.num_kv_heads = s->cfg.num_kv_heads;
+        p.head_dim = s->cfg.head_dim;
+        p.tokens = s->seq_tokens[seq];
+        p.seed = seed;
+        p.logical_seq = logical_seq;
+        p.logical_tok0 = logical_tok0;
+        p.amp_k = amp_k;
+        p.amp_v = amp_v;
+        if (p.tokens == 0) return;
+        cuda_check(launch_fill_kv(s->cfg.dtype, s->dp, p, s->stream), "launch(fill_kv)");
+        count_launch(1);
+    });
+}
+
+dattn_status dattn_q_fill_synthetic(dattn_store* s, void* q_dev, int rows, uint64_t seed,
+                                    uint32_t row0, float amp_q) {
+    return guarded([&] {
+        REQUIRE_ARG(s && q_dev, "null argument");
+        if (rows <= 0) return;
+        s->activate();
+        QFillParams p{q_dev, rows, s->cfg.num_q_heads, s->cfg.head_dim, seed, row0, amp_q};
+        cuda_check(launch_fill_q(s->cfg.dtype, s->dp, p, s->stream), "launch(fill_q)");
+        count_launch(1);
+    });
+}
+
+dattn_status dattn_decode(dattn_store* s, const dattn_batch* b, const void* q, void* out,
+                          void* row_partials, int mem) {
+    return guarded([&] {
+        REQUIRE_ARG(s && b, "null argument");
+        REQUIRE_ARG(q || b->num_rows == 0, "null queries");
+        REQUIRE_ARG(mem == DATTN_MEM_DEVICE || mem == DATTN_MEM_HOST, "bad mem kind");
+        s->decode(*b, q, out, row_partials, mem);
+    });
+}
+
+dattn_status dattn_micro_attention(dattn_store* s, const dattn_batch* b, const void* q_dev,
+                                   void* partials_dev) {
+    return guarded([&] {
+        REQUIRE_ARG(s && b && partials_dev, "null argument");
+        REQUIRE_ARG(q_dev || b->num_rows == 0, "null queries");
+        s->micro_attention(*b, q_dev, partials_dev);
+    });
+}
+
+dattn_status dattn_merge_partials(dattn_store* s, const dattn_merge_desc* d, const void* recs,
+                                  void* out_recs, void* out_norm) {
+    return guarded([&] {
+        REQUIRE_ARG(s && d && recs, "null argument");
+        if (d->rows < 0 || d->heads < 1) throw Error(DATTN_ERR_CONTRACT, "bad merge shape");
+        s->activate();
+        MergeParams mp{};
+        mp.recs = recs;
+        mp.rows = d->rows;
+        mp.heads = d->heads;
+        mp.row_begin = d->row_begin;
+        mp.n_uniform = d->n_uniform;
+        mp.row_mul = d->row_mul;
+        mp.c_stride = d->c_stride;
+        mp.group = s->group;
+        mp.out_recs = out_recs;
+        mp.out_norm = out_norm;
+        s->run_merge(mp);
+    });
+}
+
+dattn_status dattn_comm_unique_id(unsigned char id[DATTN_UNIQUE_ID_BYTES]) {
+    return guarded([&] {
+        REQUIRE_ARG(id, "null argument");
+        static_assert(sizeof(ncclUniqueId) == DATTN_UNIQUE_ID_BYTES, "nccl id size");
+        ncclUniqueId u;
+        nccl_check(ncclGetUniqueId(&u), "ncclGetUniqueId");
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE_ID_BYTES],
+                             int rank, int nranks) {
+    return guarded([&] {
+        REQUIRE_ARG(s && id, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            throw Error(DATTN_ERR_CONTRACT, "bad rank / world size");
+        s->activate();
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        if (s->comm) ncclCommDestroy(s->comm);
+        s->comm = nullptr;
+        nccl_check(ncclCommInitRank(&s->comm, nranks, u, rank), "ncclCommInitRank");
+        s->rank = rank;
+        s->nranks = nranks;
+    });
+}
+
+dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const void* q, void* out,
+                                  int mem) {
+    return guarded([&] {
+        REQUIRE_ARG(s && b && out, "null argument");
+        REQUIRE_ARG(q || b->num_rows == 0, "null queries");
+        REQUIRE_ARG(mem == DATTN_MEM_DEVICE || mem == DATTN_MEM_HOST, "bad mem kind");
+        s->decode_sharded(*b, q, out, mem);
+    });
+}
+
+dattn_status dattn_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        REQUIRE_ARG(out, "null argument");
+        cuda_check(cudaMallocHost(out, std::max<size_t>(bytes, 1)), "cudaMallocHost");
+    });
+}
+void dattn_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+dattn_status dattn_device_alloc(dattn_store* s, size_t bytes, void** out) {
+    return guarded([&] {
+        REQUIRE_ARG(s && out, "null argument");
+        s->activate();
+        cuda_check(cudaMalloc(out, std::max<size_t>(bytes, 1)), "cudaMalloc");
+    });
+}
+void dattn_device_free(dattn_store* s, void* p) {
+    if (!p) return;
+    if (s) cudaSetDevice(s->cfg.device);
+    cudaFree(p);
+}
+dattn_status dattn_memcpy(dattn_store* s, void* dst, const void* src, size_t bytes, int kind) {
+    return guarded([&] {
+        REQUIRE_ARG(s && (bytes == 0 || (dst && src)), "null argument");
+        s->activate();
+        cuda_check(cudaMemcpyAsync(dst, src, bytes, static_cast<cudaMemcpyKind>(kind), s->stream),
+                   "cudaMemcpyAsync");
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    });
+}
+
+}  // extern "C"

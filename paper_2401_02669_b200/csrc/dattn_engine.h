@@ -1,0 +1,122 @@
+// dattn_engine.h -- host-side engine objects behind the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dattn.h"
+#include "dattn_internal.h"
+
+namespace dattn {
+
+struct Error : std::runtime_error {
+    Error(dattn_status s, const std::string& m);
+    dattn_status status;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+void set_error(const std::string& s);
+void count_launch(int n);
+int padded_dim_for(int head_dim);
+int elem_bytes_for(int dtype);
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes);
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf();
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes);
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf();
+};
+
+// Decode plan: the int32 metadata block uploaded once per call.
+struct Plan {
+    std::vector<int32_t> words;
+    size_t off_ranges = 0, off_item = 0, off_chunk = 0, off_rowchunk = 0, off_kvh = 0;
+    int32_t nitems = 0, nchunks = 0, nranges = 0, nrows = 0, chunk_tokens = 0;
+    bool any_kvh = false;
+};
+
+}  // namespace dattn
+
+struct dattn_store {
+    dattn_store_config cfg{};
+    int dp = 0, esz = 0, acc_sz = 0, rec_elems = 0, group = 1;
+    int64_t page_elems = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t meta_ev = nullptr;
+    int num_sms = 0;
+    int ma_stages = 0, ma_ctas_per_sm = 1;
+    size_t ma_smem = 0;
+
+    void* kpool = nullptr;
+    void* vpool = nullptr;
+    int32_t* d_bt = nullptr;
+    int32_t* d_counter = nullptr;
+    int32_t* d_flag = nullptr;
+
+    // page ledger (RManager::alloc_local / free_request, controlplane.cpp:38-79)
+    std::vector<int32_t> h_bt;
+    std::vector<int64_t> seq_tokens;
+    std::vector<int32_t> seq_pages;
+    std::vector<uint8_t> seq_live;
+    std::vector<int32_t> free_pages;
+    std::vector<int32_t> free_seqs;
+    int64_t used_pages = 0;
+
+    dattn::DevBuf d_meta, recs, rowrecs, qbuf, obuf, gathered, d_staging;
+    dattn::HostBuf h_meta, h_staging;
+    size_t staging_used = 0;
+    dattn::Plan scratch_plan;
+
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+
+    bool timing = false;
+    dattn_stats stats{};
+    std::vector<std::array<cudaEvent_t, 2>> ma_events, merge_events;
+    size_t ma_events_used = 0, merge_events_used = 0;
+    cudaEvent_t* timer_pair(int kind);
+    void collect_timing();
+
+    ~dattn_store();
+    void init(const dattn_store_config& c);
+    void activate() const;
+    void check_seq(int32_t seq) const;
+    void grow(int32_t seq, int64_t tokens);
+    void upload_bt_row(int32_t seq);
+    void write_rows(int32_t seq, int kv_head, int64_t tok0, int64_t n, const void* k,
+                    const void* v, int src_dtype, int src_row_elems);
+
+    void plan(const dattn_batch& b, bool one_chunk_per_range, dattn::Plan& pl) const;
+    void upload_plan(const dattn::Plan& pl);
+    void run_ma(const dattn::Plan& pl, const void* q_dev, void* recs, double scale,
+                bool check_finite);
+    void run_merge(const dattn::MergeParams& mp);
+    void local_merge(const dattn::Plan& pl, const void* recs, void* out_recs, void* out_norm);
+    void check_flag();
+    double effective_scale() const;
+    size_t q_bytes(int rows) const;
+    size_t rec_bytes() const;
+
+    void decode(const dattn_batch& b, const void* q, void* out, void* row_partials, int mem);
+    void micro_attention(const dattn_batch& b, const void* q_dev, void* partials);
+    void decode_sharded(const dattn_batch& b, const void* q, void* out, int mem);
+};

@@ -1,0 +1,113 @@
+// dattn_internal.h -- kernel parameter blocks and launchers shared by the
+// CUDA kernels (dattn_kernels.cu) and the host engine (dattn_engine.cpp).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dattn {
+
+// One decode range as the kernels see it (host dattn_range, narrowed).
+struct RangeDev {
+    int32_t seq;
+    int32_t out_row;
+    int32_t kv_head;  // -1: all kv heads
+    int32_t lo;
+    int32_t hi;
+    int32_t pad[3];
+};
+
+// K1 micro-attention launch.
+struct MAParams {
+    const void* k_pool;  // [pages][Hkv][P][DP]
+    const void* v_pool;
+    const int32_t* block_tables;  // [max_seqs][bt_stride]
+    int32_t bt_stride;
+    int32_t page_tokens;
+    int32_t num_kv_heads;
+    int32_t num_q_heads;
+    int32_t group;  // Hq / Hkv
+    const void* q;  // [rows][Hq][DP]
+    const RangeDev* ranges;
+    const int32_t* item_prefix;   // nranges+1
+    const int32_t* chunk_prefix;  // nranges+1
+    int32_t nranges;
+    int32_t nitems;
+    int32_t chunk_tokens;
+    double scale_log2;  // scale * log2(e)
+    void* records;      // [chunks][Hq][DP+4] accumulation type
+    int32_t* work_counter;
+    int32_t* nonfinite_flag;  // may be null
+    int32_t stages;
+};
+
+// K3 merge launch.
+struct MergeParams {
+    const void* recs;
+    int32_t rows;
+    int32_t heads;
+    const int32_t* row_begin;  // rows+1 or null
+    int32_t n_uniform;
+    int64_t row_mul;
+    int64_t c_stride;
+    const int32_t* chunk_kvh;  // per (row_begin[row]+c) kv head tag (-1 all) or null
+    int32_t group;             // q heads per kv head, for chunk_kvh
+    void* out_recs;            // [rows*heads][DP+4] or null
+    void* out_norm;            // [rows*heads][DP] storage dtype, or null
+};
+
+struct FillParams {
+    void* k_pool;
+    void* v_pool;
+    const int32_t* block_row;  // block-table row of the sequence
+    int32_t page_tokens;
+    int32_t num_kv_heads;
+    int32_t head_dim;
+    int64_t tokens;
+    uint64_t seed;
+    uint32_t logical_seq;
+    int64_t logical_tok0;
+    float amp_k;
+    float amp_v;
+};
+
+struct QFillParams {
+    void* q;
+    int32_t rows;
+    int32_t heads;
+    int32_t head_dim;
+    uint64_t seed;
+    uint32_t row0;
+    float amp;
+};
+
+struct ScatterParams {
+    void* k_pool;
+    void* v_pool;
+    const void* k_rows;  // [n][DP]
+    const void* v_rows;
+    const int32_t* block_row;
+    int32_t page_tokens;
+    int32_t num_kv_heads;
+    int32_t kv_head;
+    int64_t tok0;
+    int64_t n;
+};
+
+// dtype codes as dattn.h
+constexpr int kBF16 = 0, kF32 = 1, kF64 = 2;
+
+int ma_threads();
+size_t ma_smem_bytes(int dtype, int dp, int group, int stages);
+int ma_stage_tokens(int dtype, int dp);
+cudaError_t ma_configure(int dtype, int dp, int group, size_t smem);
+cudaError_t ma_occupancy(int dtype, int dp, int group, size_t smem, int* blocks_per_sm);
+cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t smem,
+                      cudaStream_t st);
+cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
+cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st);
+cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);
+cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
+cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
+cudaError_t launch_identity_records(int dtype, int dp, void* recs, int64_t n, cudaStream_t st);
+
+}  // namespace dattn

@@ -1,0 +1,795 @@
+// dattn_kernels.cu -- sm_100a kernels of the DistAttention decode path.
+//
+//   K1 ma_decode_kernel   micro-attention partials (m, e, ma) per
+//                         (chunk, q head): compute_micro_attention,
+//                         /root/reference/proj/src/distattention.cpp:99-129,
+//                         batched over a paged KV store.
+//   K3 merge_kernel       online-softmax rescale-and-sum of partial records:
+//                         combine_partials / aggregate_partials,
+//                         distattention.cpp:131-174.
+//   K4 fill_kv_kernel     deterministic counter-hash K/V generation into pages
+//                         (CPU twin: oracle/dattn_oracle.c or_synth_kv).
+//
+// K1 design: persistent CTAs, one producer warp whose elected
+// lane streams each work item's K/V token rows from the page pool into a ring
+// of shared-memory stages with 1-D bulk TMA (cp.async.bulk, mbarrier
+// complete_tx, L2 evict_first), and 8 consumer warps that read 16-B chunks
+// from shared memory (8 lanes per token row, conflict-free LDS.128), reduce
+// q.k with warp shuffles and run an online softmax in registers. Work items
+// (range, chunk, kv head) are claimed with an atomic counter so ragged
+// batches balance across the 148 SMs.
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+#include <type_traits>
+
+#include "dattn_internal.h"
+#include "dattn_ptx.cuh"
+
+namespace dattn {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kMAThreads = 32 * (1 + kConsumerWarps);
+constexpr int kStageSlotBytes = 16384;  // bytes of K (and of V) per pipeline stage
+constexpr int kPidWindow = 256;         // block-table entries cached per window
+
+int ma_threads() { return kMAThreads; }
+
+template <typename T, int DP>
+struct Shape {
+    static constexpr int kRowBytes = DP * static_cast<int>(sizeof(T));
+    static constexpr int kChunks = kRowBytes / 16;               // 16-B chunks per row
+    static constexpr int kLPT = kChunks < 8 ? kChunks : 8;       // lanes per token row
+    static constexpr int kTPW = 32 / kLPT;                       // token rows per warp pass
+    static constexpr int kCPL = kChunks / kLPT;                  // chunks per lane
+    static constexpr int kVec = 16 / static_cast<int>(sizeof(T));
+    static constexpr int kEPL = kCPL * kVec;                     // elements per lane
+    static constexpr int kRawStage = kStageSlotBytes / kRowBytes;
+    static constexpr int kStageTokens = kRawStage < 8 ? 8 : (kRawStage > 512 ? 512 : kRawStage);
+    static constexpr int kPassTokens = kConsumerWarps * kTPW;
+    static constexpr int kUnrollRaw = kStageTokens / kPassTokens;
+    static constexpr int kUnroll = kUnrollRaw < 1 ? 1 : (kUnrollRaw > 4 ? 4 : kUnrollRaw);
+    static constexpr int kRec = DP + 4;
+};
+
+struct StageMeta {
+    int32_t item;  // -1: terminate
+    int32_t ntok;
+    int32_t flags;  // 1 first stage of item, 2 last stage
+    int32_t row;
+    int32_t kvh;
+    int32_t gchunk;
+    int32_t item_tokens;
+    int32_t pad;
+};
+
+__host__ __device__ constexpr size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Shared-memory carve-up, identical on host and device.
+template <typename T, int DP>
+struct Layout {
+    using Acc = typename Elem<T>::Acc;
+    size_t bars, meta, pid, red_m, red_e, red_acc, stage0, stage_bytes, k_off, v_off, q_off,
+        total;
+    __host__ __device__ Layout(int stages, int group) {
+        using S = Shape<T, DP>;
+        size_t o = 0;
+        bars = o;
+        o += sizeof(uint64_t) * 2 * stages;
+        o = align_up(o, 16);
+        meta = o;
+        o += sizeof(StageMeta) * stages;
+        pid = o;
+        o += sizeof(int32_t) * kPidWindow;
+        o = align_up(o, 16);
+        red_m = o;
+        o += sizeof(Acc) * kConsumerWarps;
+        red_e = o;
+        o += sizeof(Acc) * kConsumerWarps;
+        o = align_up(o, 16);
+        red_acc = o;
+        o += sizeof(Acc) * kConsumerWarps * DP;
+        o = align_up(o, 128);
+        stage0 = o;
+        k_off = 0;
+        v_off = align_up(static_cast<size_t>(S::kStageTokens) * S::kRowBytes, 128);
+        q_off = v_off + v_off;
+        stage_bytes = align_up(q_off + static_cast<size_t>(group) * S::kRowBytes, 128);
+        total = stage0 + stage_bytes * stages;
+    }
+};
+
+__device__ __forceinline__ int find_range(const int32_t* prefix, int n, int item) {
+    // largest r with prefix[r] <= item (prefix[0] == 0, prefix[n] > item)
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(prefix + mid) <= item) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T, int DP, int HPW>
+__global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 2)
+    ma_decode_kernel(const MAParams p) {
+    using S = Shape<T, DP>;
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int LPT = S::kLPT, TPW = S::kTPW, CPL = S::kCPL, VEC = S::kVec, EPL = S::kEPL;
+    constexpr int TS = S::kStageTokens, U = S::kUnroll, REC = S::kRec;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    const Layout<T, DP> L(p.stages, p.group);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* empty = full + p.stages;
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta);
+    int32_t* pid = reinterpret_cast<int32_t*>(smem + L.pid);
+    Acc* red_m = reinterpret_cast<Acc*>(smem + L.red_m);
+    Acc* red_e = reinterpret_cast<Acc*>(smem + L.red_e);
+    Acc* red_acc = reinterpret_cast<Acc*>(smem + L.red_acc);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int stages = p.stages;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ===================== producer warp =====================
+        const uint64_t pol = l2_policy_evict_first();
+        const T* kpool = static_cast<const T*>(p.k_pool);
+        const T* vpool = static_cast<const T*>(p.v_pool);
+        const T* qg = static_cast<const T*>(p.q);
+        const int P = p.page_tokens;
+        const uint32_t qbytes = static_cast<uint32_t>(p.group) * S::kRowBytes;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            int item = 0;
+            if (lane == 0) item = atomicAdd(p.work_counter, 1);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= p.nitems) break;
+            const int r = find_range(p.item_prefix, p.nranges, item);
+            const RangeDev rg = p.ranges[r];
+            const int local = item - __ldg(p.item_prefix + r);
+            const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
+            const int j = local / nh;
+            const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
+            const int tlo = rg.lo + j * p.chunk_tokens;
+            const int thi = min(rg.hi, tlo + p.chunk_tokens);
+            const int gchunk = __ldg(p.chunk_prefix + r) + j;
+            const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
+            int win_lo = -1;
+            for (int t0 = tlo; t0 < thi; t0 += TS) {
+                const int n = min(TS, thi - t0);
+                const int pf = t0 / P, pl = (t0 + n - 1) / P;
+                if (win_lo < 0 || pl >= win_lo + kPidWindow) {
+                    __syncwarp();
+                    win_lo = pf;
+                    const int plast = (thi - 1) / P;
+                    for (int i = lane; i < kPidWindow; i += 32)
+                        if (win_lo + i <= plast) pid[i] = __ldg(bt + win_lo + i);
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    const bool first = (t0 == tlo);
+                    StageMeta& md = meta[stage];
+                    md.item = item;
+                    md.ntok = n;
+                    md.flags = (first ? 1 : 0) | (t0 + TS >= thi ? 2 : 0);
+                    md.row = rg.out_row;
+                    md.kvh = kvh;
+                    md.gchunk = gchunk;
+                    md.item_tokens = thi - tlo;
+                    uint8_t* sb = smem + L.stage0 + L.stage_bytes * stage;
+                    T* ks = reinterpret_cast<T*>(sb + L.k_off);
+                    T* vs = reinterpret_cast<T*>(sb + L.v_off);
+                    mbar_arrive_expect_tx(&full[stage],
+                                          2u * n * S::kRowBytes + (first ? qbytes : 0u));
+                    for (int t = t0; t < t0 + n;) {
+                        const int pi = t / P;
+                        const int off = t - pi * P;
+                        const int cnt = min(P - off, t0 + n - t);
+                        const int64_t page = pid[pi - win_lo];
+                        const int64_t row = (page * p.num_kv_heads + kvh) * P + off;
+                        const uint32_t bytes = static_cast<uint32_t>(cnt) * S::kRowBytes;
+                        bulk_g2s(ks + static_cast<int64_t>(t - t0) * DP, kpool + row * DP, bytes,
+                                 &full[stage], pol);
+                        bulk_g2s(vs + static_cast<int64_t>(t - t0) * DP, vpool + row * DP, bytes,
+                                 &full[stage], pol);
+                        t += cnt;
+                    }
+                    if (first) {
+                        const T* qsrc =
+                            qg + (static_cast<int64_t>(rg.out_row) * p.num_q_heads +
+                                  static_cast<int64_t>(kvh) * p.group) * DP;
+                        bulk_g2s_nohint(sb + L.q_off, qsrc, qbytes, &full[stage]);
+                    }
+                }
+                __syncwarp();
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            meta[stage].item = -1;
+            mbar_arrive(&full[stage]);
+        }
+        return;
+    }
+
+    // ===================== consumer warps =====================
+    const int cw = warp - 1;
+    const int gslots = p.group < kConsumerWarps ? p.group : kConsumerWarps;
+    const int wph = kConsumerWarps / gslots;  // warps sharing one q head
+    const bool active = cw < wph * gslots;
+    const int hslot = cw % gslots;
+    const int slice = cw / gslots;
+    const int grp = lane / LPT;
+    const int sub = lane - grp * LPT;
+    const Acc scale_log2 = static_cast<Acc>(p.scale_log2);
+    const Acc kLn2 = static_cast<Acc>(0.6931471805599453094);
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    bool nonfinite = false;
+
+    Acc q[HPW][EPL];
+    Acc acc[HPW][EPL];
+    Acc m[HPW], e[HPW];
+#pragma unroll
+    for (int hs = 0; hs < HPW; ++hs) {
+        m[hs] = kNegInf;
+        e[hs] = 0;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) q[hs][i] = acc[hs][i] = 0;
+    }
+
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+        mbar_wait(&full[stage], phase);
+        const StageMeta md = meta[stage];
+        if (md.item < 0) break;
+        const uint8_t* sb = smem + L.stage0 + L.stage_bytes * stage;
+        const T* ks = reinterpret_cast<const T*>(sb + L.k_off);
+        const T* vs = reinterpret_cast<const T*>(sb + L.v_off);
+        if (md.flags & 1) {
+            const T* qs = reinterpret_cast<const T*>(sb + L.q_off);
+#pragma unroll
+            for (int hs = 0; hs < HPW; ++hs) {
+                const int h = hslot + hs * gslots;
+                const bool hv = active && h < p.group;
+#pragma unroll
+                for (int c = 0; c < CPL; ++c)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v)
+                        q[hs][c * VEC + v] =
+                            hv ? E::to_acc(qs[h * DP + (c * LPT + sub) * VEC + v]) * scale_log2
+                               : Acc(0);
+                m[hs] = kNegInf;
+                e[hs] = 0;
+#pragma unroll
+                for (int i = 0; i < EPL; ++i) acc[hs][i] = 0;
+            }
+        }
+        if (active) {
+            const int n = md.ntok;
+            for (int base = slice * TPW; base < n; base += wph * TPW * U) {
+                Acc s[U][HPW];
+                bool valid[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = base + u * wph * TPW + grp;
+                    valid[u] = t < n;
+                    const int tc = valid[u] ? t : n - 1;
+                    const uint4* rowp = reinterpret_cast<const uint4*>(ks + tc * DP);
+#pragma unroll
+                    for (int hs = 0; hs < HPW; ++hs) s[u][hs] = 0;
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        const uint4 ch = rowp[c * LPT + sub];
+                        Acc x[VEC];
+                        E::unpack(ch, x);
+                        if constexpr (std::is_same<T, double>::value) {
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) nonfinite |= !isfinite(x[v]);
+                        }
+#pragma unroll
+                        for (int hs = 0; hs < HPW; ++hs)
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) s[u][hs] += q[hs][c * VEC + v] * x[v];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int hs = 0; hs < HPW; ++hs)
+#pragma unroll
+                        for (int off = 1; off < LPT; off <<= 1)
+                            s[u][hs] += __shfl_xor_sync(0xffffffffu, s[u][hs], off);
+                Acc pw[U][HPW];
+#pragma unroll
+                for (int hs = 0; hs < HPW; ++hs) {
+                    Acc mx = m[hs];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (valid[u]) mx = s[u][hs] > mx ? s[u][hs] : mx;
+                    const Acc corr = (mx == m[hs]) ? Acc(1) : acc_exp2(m[hs] - mx);
+                    Acc es = e[hs] * corr;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        pw[u][hs] = valid[u] ? acc_exp2(s[u][hs] - mx) : Acc(0);
+                        es += pw[u][hs];
+                    }
+                    e[hs] = es;
+                    m[hs] = mx;
+#pragma unroll
+                    for (int i = 0; i < EPL; ++i) acc[hs][i] *= corr;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!valid[u]) continue;
+                    const int t = base + u * wph * TPW + grp;
+                    const uint4* rowp = reinterpret_cast<const uint4*>(vs + t * DP);
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        const uint4 ch = rowp[c * LPT + sub];
+                        Acc x[VEC];
+                        E::unpack(ch, x);
+                        if constexpr (std::is_same<T, double>::value) {
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) nonfinite |= !isfinite(x[v]);
+                        }
+#pragma unroll
+                        for (int hs = 0; hs < HPW; ++hs)
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v)
+                                acc[hs][c * VEC + v] += pw[u][hs] * x[v];
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+
+        if (md.flags & 2) {
+            // ---- finalize the item: merge token groups inside the warp ----
+#pragma unroll
+            for (int hs = 0; hs < HPW; ++hs) {
+#pragma unroll
+                for (int off = LPT; off < 32; off <<= 1) {
+                    const Acc mo = __shfl_xor_sync(0xffffffffu, m[hs], off);
+                    const Acc eo = __shfl_xor_sync(0xffffffffu, e[hs], off);
+                    const Acc mn = mo > m[hs] ? mo : m[hs];
+                    const Acc c1 = (m[hs] == mn) ? Acc(1) : acc_exp2(m[hs] - mn);
+                    const Acc c2 = (mo == mn) ? Acc(1) : acc_exp2(mo - mn);
+                    e[hs] = e[hs] * c1 + eo * c2;
+#pragma unroll
+                    for (int i = 0; i < EPL; ++i) {
+                        const Acc ao = __shfl_xor_sync(0xffffffffu, acc[hs][i], off);
+                        acc[hs][i] = acc[hs][i] * c1 + ao * c2;
+                    }
+                    m[hs] = mn;
+                }
+            }
+            Acc* recs = static_cast<Acc*>(p.records);
+            const int64_t rec_base =
+                static_cast<int64_t>(md.gchunk) * p.num_q_heads + static_cast<int64_t>(md.kvh) * p.group;
+            if (wph == 1) {
+#pragma unroll
+                for (int hs = 0; hs < HPW; ++hs) {
+                    const int h = hslot + hs * gslots;
+                    if (!active || h >= p.group) continue;
+                    Acc* rec = recs + (rec_base + h) * REC;
+                    if (grp == 0) {
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v)
+                                rec[4 + (c * LPT + sub) * VEC + v] = acc[hs][c * VEC + v];
+                    }
+                    if (lane == 0) {
+                        rec[0] = m[hs] * kLn2;
+                        rec[1] = e[hs];
+                        rec[2] = static_cast<Acc>(md.item_tokens);
+                        rec[3] = 0;
+                    }
+                }
+            } else {
+                // several warps per head: reduce through shared memory
+                if (grp == 0) {
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v)
+                            red_acc[cw * DP + (c * LPT + sub) * VEC + v] = acc[0][c * VEC + v];
+                }
+                if (lane == 0) {
+                    red_m[cw] = m[0];
+                    red_e[cw] = e[0];
+                }
+                named_bar_sync(1, 32 * kConsumerWarps);
+                if (active && slice == 0 && hslot < p.group) {
+                    Acc mg = kNegInf;
+                    for (int s2 = 0; s2 < wph; ++s2) {
+                        const Acc mm = red_m[hslot + s2 * gslots];
+                        mg = mm > mg ? mm : mg;
+                    }
+                    Acc wt[kConsumerWarps];
+                    Acc eg = 0;
+#pragma unroll
+                    for (int s2 = 0; s2 < kConsumerWarps; ++s2) {
+                        if (s2 < wph) {
+                            const Acc mm = red_m[hslot + s2 * gslots];
+                            wt[s2] = (mm == mg) ? Acc(1) : acc_exp2(mm - mg);
+                            eg += red_e[hslot + s2 * gslots] * wt[s2];
+                        } else {
+                            wt[s2] = 0;
+                        }
+                    }
+                    Acc* rec = recs + (rec_base + hslot) * REC;
+                    for (int jd = lane; jd < DP; jd += 32) {
+                        Acc a = 0;
+#pragma unroll
+                        for (int s2 = 0; s2 < kConsumerWarps; ++s2)
+                            if (s2 < wph) a += red_acc[(hslot + s2 * gslots) * DP + jd] * wt[s2];
+                        rec[4 + jd] = a;
+                    }
+                    if (lane == 0) {
+                        rec[0] = mg * kLn2;
+                        rec[1] = eg;
+                        rec[2] = static_cast<Acc>(md.item_tokens);
+                        rec[3] = 0;
+                    }
+                }
+                named_bar_sync(1, 32 * kConsumerWarps);
+            }
+        }
+        if (++stage == stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+    if (nonfinite && p.nonfinite_flag) atomicOr(p.nonfinite_flag, 1);
+}
+
+// ------------------------------------------------------------------ K3
+template <typename T, int DP>
+__global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int REC = DP + 4;
+    constexpr int EPL = (DP + 31) / 32;
+    const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= static_cast<int64_t>(p.rows) * p.heads) return;
+    const int row = static_cast<int>(g / p.heads);
+    const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
+    int n;
+    int64_t base;
+    int cbase = 0;
+    if (p.row_begin) {
+        cbase = p.row_begin[row];
+        n = p.row_begin[row + 1] - cbase;
+        base = static_cast<int64_t>(cbase) * p.row_mul + h;
+    } else {
+        n = p.n_uniform;
+        base = static_cast<int64_t>(row) * p.row_mul + h;
+    }
+    const int my_kvh = p.chunk_kvh ? h / p.group : 0;
+    const Acc* R = static_cast<const Acc*>(p.recs);
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+
+    Acc mg = kNegInf;
+    for (int c = lane; c < n; c += 32) {
+        if (p.chunk_kvh) {
+            const int tag = p.chunk_kvh[cbase + c];
+            if (tag >= 0 && tag != my_kvh) continue;
+        }
+        const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+        if (r[2] != Acc(0)) mg = r[0] > mg ? r[0] : mg;  // live (tokens > 0) records only
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+        mg = o > mg ? o : mg;
+    }
+    Acc eg = 0, ntok = 0;
+    Acc acc[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) acc[k] = 0;
+    for (int c = 0; c < n; ++c) {
+        if (p.chunk_kvh) {
+            const int tag = p.chunk_kvh[cbase + c];
+            if (tag >= 0 && tag != my_kvh) continue;
+        }
+        const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+        if (r[2] == Acc(0)) continue;  // identity (seq_p == 0): skipped, never rescaled
+        const Acc ec = r[1];
+        const Acc mc = r[0];
+        const Acc w = (mc == mg) ? Acc(1) : exp(mc - mg);
+        eg += ec * w;
+        ntok += r[2];
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+            const int j = lane + 32 * k;
+            if (j < DP) acc[k] += r[4 + j] * w;
+        }
+    }
+    if (p.out_recs) {
+        Acc* o = static_cast<Acc*>(p.out_recs) + g * REC;
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+            const int j = lane + 32 * k;
+            if (j < DP) o[4 + j] = acc[k];
+        }
+        if (lane == 0) {
+            o[0] = ntok != Acc(0) ? mg : kNegInf;
+            o[1] = eg;
+            o[2] = ntok;
+            o[3] = 0;
+        }
+    }
+    if (p.out_norm) {
+        T* o = static_cast<T*>(p.out_norm) + g * DP;
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+            const int j = lane + 32 * k;
+            if (j < DP) o[j] = E::from_acc(ntok != Acc(0) ? acc[k] / eg : Acc(0));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K4
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t stream_key(uint64_t seed, int tensor) {
+    return splitmix64(seed ^ (static_cast<uint64_t>(tensor) * 0xD1B54A32D192ED03ull));
+}
+__device__ __forceinline__ uint64_t elem_index(uint32_t seq, uint32_t head, uint32_t token,
+                                               uint32_t dim) {
+    return (static_cast<uint64_t>(seq) << 40) | (static_cast<uint64_t>(head & 0xFFu) << 32) |
+           (static_cast<uint64_t>(token & 0xFFFFFFu) << 8) | static_cast<uint64_t>(dim & 0xFFu);
+}
+__device__ __forceinline__ float synth_f32(uint64_t key, uint64_t idx, float amp) {
+    const uint32_t u24 = static_cast<uint32_t>(splitmix64(key ^ idx) >> 40);
+    const float a = static_cast<float>(static_cast<int32_t>(u24) - (1 << 23));
+    return __fmul_rn(a, __fmul_rn(amp, 0x1.0p-23f));
+}
+template <typename T>
+__device__ __forceinline__ T store_as(float x) {
+    if constexpr (std::is_same<T, bf16_t>::value) return Elem<bf16_t>::from_acc(x);
+    else return static_cast<T>(x);
+}
+
+template <typename T, int DP>
+__global__ void fill_kv_kernel(const FillParams p) {
+    const uint64_t kk = stream_key(p.seed, 1), kv = stream_key(p.seed, 2);
+    const int64_t total = p.tokens * p.num_kv_heads * DP;
+    T* kp = static_cast<T*>(p.k_pool);
+    T* vp = static_cast<T*>(p.v_pool);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % DP);
+        const int64_t th = i / DP;
+        const int h = static_cast<int>(th % p.num_kv_heads);
+        const int64_t t = th / p.num_kv_heads;
+        const int64_t page = p.block_row[t / p.page_tokens];
+        const int64_t dst = ((page * p.num_kv_heads + h) * p.page_tokens + t % p.page_tokens) * DP + j;
+        if (j < p.head_dim) {
+            const uint64_t ix = elem_index(p.logical_seq, h, static_cast<uint32_t>(p.logical_tok0 + t), j);
+            kp[dst] = store_as<T>(synth_f32(kk, ix, p.amp_k));
+            vp[dst] = store_as<T>(synth_f32(kv, ix, p.amp_v));
+        } else {
+            kp[dst] = store_as<T>(0.f);
+            vp[dst] = store_as<T>(0.f);
+        }
+    }
+}
+
+template <typename T, int DP>
+__global__ void fill_q_kernel(const QFillParams p) {
+    const uint64_t kq = stream_key(p.seed, 3);
+    const int64_t total = static_cast<int64_t>(p.rows) * p.heads * DP;
+    T* q = static_cast<T*>(p.q);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % DP);
+        const int64_t rh = i / DP;
+        const int h = static_cast<int>(rh % p.heads);
+        const uint32_t row = static_cast<uint32_t>(rh / p.heads) + p.row0;
+        q[i] = j < p.head_dim ? store_as<T>(synth_f32(kq, elem_index(row, h, 0, j), p.amp))
+                              : store_as<T>(0.f);
+    }
+}
+
+template <typename T, int DP>
+__global__ void scatter_kernel(const ScatterParams p) {
+    const int64_t total = p.n * DP;
+    const T* ks = static_cast<const T*>(p.k_rows);
+    const T* vs = static_cast<const T*>(p.v_rows);
+    T* kp = static_cast<T*>(p.k_pool);
+    T* vp = static_cast<T*>(p.v_pool);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % DP);
+        const int64_t t = p.tok0 + i / DP;
+        const int64_t page = p.block_row[t / p.page_tokens];
+        const int64_t dst =
+            ((page * p.num_kv_heads + p.kv_head) * p.page_tokens + t % p.page_tokens) * DP + j;
+        kp[dst] = ks[i];
+        vp[dst] = vs[i];
+    }
+}
+
+template <typename T, int DP>
+__global__ void gather_kernel(const ScatterParams p) {
+    const int64_t total = p.n * DP;
+    T* ks = static_cast<T*>(const_cast<void*>(p.k_rows));
+    T* vs = static_cast<T*>(const_cast<void*>(p.v_rows));
+    const T* kp = static_cast<const T*>(p.k_pool);
+    const T* vp = static_cast<const T*>(p.v_pool);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % DP);
+        const int64_t t = p.tok0 + i / DP;
+        const int64_t page = p.block_row[t / p.page_tokens];
+        const int64_t src =
+            ((page * p.num_kv_heads + p.kv_head) * p.page_tokens + t % p.page_tokens) * DP + j;
+        ks[i] = kp[src];
+        vs[i] = vp[src];
+    }
+}
+
+template <typename Acc, int DP>
+__global__ void identity_records_kernel(Acc* recs, int64_t n) {
+    constexpr int REC = DP + 4;
+    const int64_t total = n * REC;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        recs[i] = (i % REC == 0) ? -static_cast<Acc>(INFINITY) : Acc(0);
+}
+
+// ------------------------------------------------------------ dispatch
+#define DATTN_DP_SWITCH(dp, ...)                      \
+    switch (dp) {                                     \
+        case 16: { constexpr int DPC = 16; __VA_ARGS__; } break;   \
+        case 32: { constexpr int DPC = 32; __VA_ARGS__; } break;   \
+        case 64: { constexpr int DPC = 64; __VA_ARGS__; } break;   \
+        case 128: { constexpr int DPC = 128; __VA_ARGS__; } break; \
+        case 256: { constexpr int DPC = 256; __VA_ARGS__; } break; \
+        default: return cudaErrorInvalidValue;        \
+    }
+#define DATTN_DT_SWITCH(dt, ...)                                 \
+    switch (dt) {                                                \
+        case kBF16: { using TC = bf16_t; __VA_ARGS__; } break;   \
+        case kF32: { using TC = float; __VA_ARGS__; } break;     \
+        case kF64: { using TC = double; __VA_ARGS__; } break;    \
+        default: return cudaErrorInvalidValue;                   \
+    }
+
+template <typename T, int DP>
+static const void* ma_fn(int group) {
+    if (group <= kConsumerWarps) return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 1>);
+    if constexpr (sizeof(T) < 8) {
+        if (group <= 2 * kConsumerWarps)
+            return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 2>);
+    }
+    return nullptr;
+}
+
+static const void* ma_kernel_ptr(int dtype, int dp, int group) {
+    const void* f = nullptr;
+    auto pick = [&]() -> cudaError_t {
+        DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, f = ma_fn<TC, DPC>(group)));
+        return cudaSuccess;
+    };
+    pick();
+    return f;
+}
+
+int ma_stage_tokens(int dtype, int dp) {
+    int ts = 0;
+    auto pick = [&]() -> cudaError_t {
+        DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, ts = (Shape<TC, DPC>::kStageTokens)));
+        return cudaSuccess;
+    };
+    pick();
+    return ts;
+}
+
+size_t ma_smem_bytes(int dtype, int dp, int group, int stages) {
+    size_t b = 0;
+    auto pick = [&]() -> cudaError_t {
+        DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, b = Layout<TC, DPC>(stages, group).total));
+        return cudaSuccess;
+    };
+    pick();
+    return b;
+}
+
+cudaError_t ma_configure(int dtype, int dp, int group, size_t smem) {
+    const void* f = ma_kernel_ptr(dtype, dp, group);
+    if (!f) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem));
+}
+
+cudaError_t ma_occupancy(int dtype, int dp, int group, size_t smem, int* blocks) {
+    const void* f = ma_kernel_ptr(dtype, dp, group);
+    if (!f) return cudaErrorInvalidValue;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, f, kMAThreads, smem);
+}
+
+cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t smem,
+                      cudaStream_t st) {
+    const void* f = ma_kernel_ptr(dtype, dp, p.group);
+    if (!f) return cudaErrorInvalidValue;
+    void* args[] = {const_cast<MAParams*>(&p)};
+    return cudaLaunchKernel(f, dim3(grid), dim3(kMAThreads), args, smem, st);
+}
+
+cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st) {
+    const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
+    if (groups == 0) return cudaSuccess;
+    const int grid = static_cast<int>((groups + 7) / 8);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+static int grid_for(int64_t total) {
+    int64_t g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st) {
+    const int grid = grid_for(p.tokens * p.num_kv_heads * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (fill_kv_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st) {
+    const int grid = grid_for(static_cast<int64_t>(p.rows) * p.heads * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (fill_q_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st) {
+    const int grid = grid_for(p.n * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (scatter_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st) {
+    const int grid = grid_for(p.n * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (gather_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_identity_records(int dtype, int dp, void* recs, int64_t n, cudaStream_t st) {
+    const int grid = grid_for(n * (dp + 4));
+    DATTN_DP_SWITCH(dp, {
+        if (dtype == kF64)
+            identity_records_kernel<double, DPC><<<grid, 256, 0, st>>>(static_cast<double*>(recs), n);
+        else
+            identity_records_kernel<float, DPC><<<grid, 256, 0, st>>>(static_cast<float*>(recs), n);
+    });
+    return cudaGetLastError();
+}
+
+}  // namespace dattn
