@@ -725,8 +725,15 @@ size_t ma_smem_bytes(int dtype, int dp, int group, int stages) {
 cudaError_t ma_configure(int dtype, int dp, int group, size_t smem) {
     const void* f = ma_kernel_ptr(dtype, dp, group);
     if (!f) return cudaErrorInvalidValue;
-    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem));
+    // One kernel serves stores of different geometries: opt in to the device
+    // maximum once instead of the last caller's size.
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    if (smem > static_cast<size_t>(optin)) return cudaErrorInvalidValue;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 cudaError_t ma_occupancy(int dtype, int dp, int group, size_t smem, int* blocks) {
