@@ -112,6 +112,8 @@ typedef struct dattn_stats {
     double ma_ms, merge_ms;     /* summed device time of timed launches */
     int64_t last_items, last_chunks, last_plan_bytes;
     int32_t last_chunk_tokens, ma_grid;
+    int32_t last_kernel;        /* 1: K1 CUDA-core MA, 2: K2 tcgen05 GQA MA */
+    int32_t reserved;
 } dattn_stats;
 dattn_status dattn_store_set_timing(dattn_store* s, int enable);
 dattn_status dattn_store_get_stats(dattn_store* s, int reset, dattn_stats* out);

@@ -92,7 +92,7 @@ class Stats(ctypes.Structure):
         ("ma_ms", ctypes.c_double), ("merge_ms", ctypes.c_double),
         ("last_items", ctypes.c_int64), ("last_chunks", ctypes.c_int64),
         ("last_plan_bytes", ctypes.c_int64), ("last_chunk_tokens", ctypes.c_int32),
-        ("ma_grid", ctypes.c_int32),
+        ("ma_grid", ctypes.c_int32), ("last_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 

@@ -168,6 +168,18 @@ void dattn_store::init(const dattn_store_config& c) {
     int occ = 0;
     cuda_check(ma_occupancy(c.dtype, dp, group, ma_smem, &occ), "occupancy(MA)");
     ma_ctas_per_sm = std::max(1, occ);
+
+    // K2: tcgen05 tiles for grouped queries (bf16, d = 128, pages dividing the 128-token tile)
+    const bool tc_shape = c.dtype == kBF16 && c.head_dim == 128 && group >= 2 && group <= 16 &&
+                          (c.page_tokens == 16 || c.page_tokens == 32 || c.page_tokens == 64 ||
+                           c.page_tokens == 128);
+    if (tc_shape && !std::getenv("DATTN_DISABLE_TC")) {
+        const uint64_t rows = static_cast<uint64_t>(c.num_pages) * c.num_kv_heads * c.page_tokens;
+        cuda_check(make_tmap_rows128(tm_k, kpool, rows, c.page_tokens), "tensor map (K pool)");
+        cuda_check(make_tmap_rows128(tm_v, vpool, rows, c.page_tokens), "tensor map (V pool)");
+        cuda_check(gqa_tc_configure(), "cudaFuncSetAttribute(K2)");
+        tc_ok = true;
+    }
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
 }
 
@@ -241,7 +253,7 @@ void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl)
         int64_t c = std::max<int64_t>(work / std::max<int64_t>(target, 1), 1);
         int64_t p2 = 1;
         while (p2 * 2 <= c) p2 *= 2;
-        const int64_t lo = std::max<int64_t>(ma_stage_tokens(cfg.dtype, dp), 64);
+        const int64_t lo = tc_ok ? 128 : std::max<int64_t>(ma_stage_tokens(cfg.dtype, dp), 64);
         C = std::min<int64_t>(std::max<int64_t>(p2, lo), 2048);
         if (C % cfg.page_tokens) C = (C / cfg.page_tokens + 1) * cfg.page_tokens;
     }
@@ -338,10 +350,26 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     p.nonfinite_flag = check_finite ? d_flag : nullptr;
     p.stages = ma_stages;
     cuda_check(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
-    const int grid = std::max(1, std::min(pl.nitems, num_sms * ma_ctas_per_sm));
+    const bool use_tc = tc_ok && !check_finite;
+    int grid;
+    if (use_tc) {
+        if (tm_q_ptr != q_dev || tm_q_rows != pl.nrows) {
+            cuda_check(make_tmap_rows128(tm_q, q_dev, static_cast<uint64_t>(std::max(pl.nrows, 1)) *
+                                                          cfg.num_q_heads, group),
+                       "tensor map (q)");
+            tm_q_ptr = q_dev;
+            tm_q_rows = pl.nrows;
+        }
+        grid = std::max(1, std::min(pl.nitems, num_sms));
+    } else {
+        grid = std::max(1, std::min(pl.nitems, num_sms * ma_ctas_per_sm));
+    }
     cudaEvent_t* ev = timing ? timer_pair(0) : nullptr;
     if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
-    cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
+    if (use_tc)
+        cuda_check(launch_gqa_tc(tm_k, tm_v, tm_q, p, grid, stream), "launch(K2 tcgen05)");
+    else
+        cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
     count_launch(1);
     stats.ma_launches++;
@@ -349,6 +377,7 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     stats.last_chunks = pl.nchunks;
     stats.last_chunk_tokens = pl.chunk_tokens;
     stats.ma_grid = grid;
+    stats.last_kernel = use_tc ? 2 : 1;
 }
 
 double dattn_store::effective_scale() const {

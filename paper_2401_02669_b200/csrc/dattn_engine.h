@@ -89,6 +89,12 @@ struct dattn_store {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
 
+    // K2 (tcgen05) path for grouped-query bf16 stores
+    bool tc_ok = false;
+    alignas(64) unsigned char tm_k[128]{}, tm_v[128]{}, tm_q[128]{};
+    const void* tm_q_ptr = nullptr;
+    int tm_q_rows = -1;
+
     bool timing = false;
     dattn_stats stats{};
     std::vector<std::array<cudaEvent_t, 2>> ma_events, merge_events;

@@ -1,0 +1,476 @@
+// dattn_gqa_tc.cu -- K2: grouped-query micro-attention on the 5th-gen tensor
+// cores (tcgen05 + TMEM + TMA), bf16 K/V, head_dim 128, 2..16 q heads per
+// kv head. Same work items, partial records and semantics as K1
+// (compute_micro_attention per chunk, /root/reference/proj/src/
+// distattention.cpp:99-129, for every q head of the kv head's group).
+//
+// Swap-AB tiles (the q group is only 8 wide, too narrow for the MMA M):
+//   MMA1  S^T[128 tok x 16] = K[128 tok x 128 d] . Q^T[128 d x 16]      (A K-major)
+//   MMA2  O^T[128 d   x 16] = V^T[128 d x 128 tok] . P^T[128 tok x 16]  (A MN-major)
+// M = 128, N = 16 (group padded with zero rows), K steps of 16, bf16 in,
+// fp32 accumulate in TMEM (32 columns). K/V pages arrive by TMA tensor copies
+// with the 128-B swizzle straight from the paged pool (box = 64 d x one
+// page), so one shared-memory copy of a tile is both the K-major A operand of
+// MMA1 and the MN-major A operand of MMA2. P^T is written by the softmax
+// warps in the same swizzled K-major layout.
+//
+// Warp roles (192 threads): w0 TMA producer, w1 TMEM owner + single-thread
+// MMA issuer, w2..w5 softmax / epilogue (thread = token row of S^T, then
+// d row of O^T). Online softmax: per-tile max across the 128 tokens through
+// shared memory, P rounded to bf16 (the same value enters e and the P.V
+// MMA), the O^T tile rescale-accumulated in registers.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "dattn_internal.h"
+#include "dattn_ptx.cuh"
+
+namespace dattn {
+namespace tc {
+
+constexpr int kTile = 128;      // tokens per tile (MMA M of MMA1)
+constexpr int kD = 128;         // head dim (MMA M of MMA2, K of MMA1)
+constexpr int kN = 16;          // MMA N: q heads, padded
+constexpr int kStages = 3;
+constexpr int kThreads = 192;
+constexpr int kHalf = kTile * 128;        // bytes of one 64-column half of a 128-row tile
+constexpr int kKVBytes = 2 * kHalf;       // one tensor (K or V) tile: 32 KB
+constexpr int kQBytes = 2 * kN * 128;     // Q slot: two halves of 16 rows x 128 B
+constexpr int kStageBytes = 2 * kKVBytes + kQBytes;  // K, V, Q = 68 KB
+constexpr int kPBytes = 2 * kN * 128;     // P^T tile
+constexpr uint32_t kTmemCols = 32;        // S^T cols 0..15, O^T cols 16..31
+
+struct StageMeta {
+    int32_t item;
+    int32_t tile0;  // sequence position of row 0 of the tile
+    int32_t tlo, thi;
+    int32_t flags;  // 1 first tile of item, 2 last tile
+    int32_t row, kvh, gchunk;
+};
+
+struct Smem {
+    uint8_t stage[kStages][kStageBytes];  // 1024-B aligned (offset 0)
+    uint8_t p[kPBytes];
+    uint64_t full[kStages], empty[kStages];
+    uint64_t s_full, s_free, p_full, o_full, o_free;
+    StageMeta meta[kStages];
+    float red_max[2][4][kN];
+    float red_sum[4][kN];
+    uint32_t tmem_base;
+};
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// UMMA shared-memory descriptor, 128-B swizzle, sm_100 version bits.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, M = 128, N = 16.
+__host__ __device__ constexpr uint32_t idesc(uint32_t a_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn_major << 15) | (0u << 16) |
+           (static_cast<uint32_t>(kN >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(id), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ int find_item_range(const int32_t* prefix, int n, int item) {
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(prefix + mid) <= item) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// byte offset of element (row, col) in a 128-B-swizzled K-major operand made of
+// two 64-column halves of `rows` rows each (half stride rows*128 B)
+__device__ __forceinline__ uint32_t swz_off(int row, int col, int rows) {
+    const int half = col >> 6;
+    const int c = (col & 63) >> 3;
+    return static_cast<uint32_t>(half * rows * 128 + (row >> 3) * 1024 + (row & 7) * 128 +
+                                 ((c ^ (row & 7)) << 4) + ((col & 7) << 1));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gqa_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                  const __grid_constant__ CUtensorMap tm_q, const MAParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // the swizzle pattern is tied to 1024-B address alignment
+    Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = p.group;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.s_full, 1);
+        mbar_init(&S.o_full, 1);
+        mbar_init(&S.s_free, 4);
+        mbar_init(&S.p_full, 4);
+        mbar_init(&S.o_free, 4);
+        fence_mbar_init();
+    }
+    // zero the operand buffers once: padded Q / P rows must be 0 and stale
+    // rows of partially filled tiles must be finite
+    for (int i = threadIdx.x; i < (kStages * kStageBytes + kPBytes) / 16; i += kThreads)
+        reinterpret_cast<uint4*>(S.stage)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&S.tmem_base)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+        prefetch_tmap(&tm_q);
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+    const uint32_t tmem_s = tmem, tmem_o = tmem + kN;
+
+    if (warp == 0) {
+        // ================================ TMA producer
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            const int P = p.page_tokens;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (;;) {
+                const int item = atomicAdd(p.work_counter, 1);
+                if (item >= p.nitems) break;
+                const int r = find_item_range(p.item_prefix, p.nranges, item);
+                const RangeDev rg = p.ranges[r];
+                const int local = item - __ldg(p.item_prefix + r);
+                const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
+                const int j = local / nh;
+                const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
+                const int tlo = rg.lo + j * p.chunk_tokens;
+                const int thi = min(rg.hi, tlo + p.chunk_tokens);
+                const int gchunk = __ldg(p.chunk_prefix + r) + j;
+                const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
+                const int start = (tlo / P) * P;
+                const int qrow = rg.out_row * p.num_q_heads + kvh * G;
+                for (int t0 = start; t0 < thi; t0 += kTile) {
+                    mbar_wait(&S.empty[stage], phase ^ 1u);
+                    StageMeta& md = S.meta[stage];
+                    md.item = item;
+                    md.tile0 = t0;
+                    md.tlo = tlo;
+                    md.thi = thi;
+                    md.flags = (t0 == start ? 1 : 0) | (t0 + kTile >= thi ? 2 : 0);
+                    md.row = rg.out_row;
+                    md.kvh = kvh;
+                    md.gchunk = gchunk;
+                    const int tend = min(thi, t0 + kTile);
+                    const int npages = (tend - 1) / P - t0 / P + 1;
+                    mbar_arrive_expect_tx(&S.full[stage],
+                                          static_cast<uint32_t>(npages * P * 128 * 4 + G * 128 * 2));
+                    uint8_t* sk = S.stage[stage];
+                    uint8_t* sv = sk + kKVBytes;
+                    uint8_t* sq = sv + kKVBytes;
+                    // independent block-table loads first (one round trip per tile)
+                    int pages[kTile / 16];
+#pragma unroll
+                    for (int pg = 0; pg < kTile / 16; ++pg)
+                        pages[pg] = pg < npages ? __ldg(bt + t0 / P + pg) : 0;
+                    for (int pg = 0; pg < npages; ++pg) {
+                        const int row0 = (pages[pg] * p.num_kv_heads + kvh) * P;
+                        const int off = pg * P * 128;
+                        tma_load_2d(sk + off, &tm_k, 0, row0, &S.full[stage], pol);
+                        tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.full[stage], pol);
+                        tma_load_2d(sv + off, &tm_v, 0, row0, &S.full[stage], pol);
+                        tma_load_2d(sv + kHalf + off, &tm_v, 64, row0, &S.full[stage], pol);
+                    }
+                    tma_load_2d(sq, &tm_q, 0, qrow, &S.full[stage], 0);
+                    tma_load_2d(sq + kN * 128, &tm_q, 64, qrow, &S.full[stage], 0);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+            mbar_wait(&S.empty[stage], phase ^ 1u);
+            S.meta[stage].item = -1;
+            mbar_arrive(&S.full[stage]);
+        }
+    } else if (warp == 1) {
+        // ================================ MMA issuer
+        const uint32_t id1 = idesc(0), id2 = idesc(1);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (uint32_t it = 0;; ++it) {
+            mbar_wait(&S.full[stage], phase);
+            const int item = S.meta[stage].item;
+            if (item < 0) break;
+            const uint32_t sk = smem_u32(S.stage[stage]);
+            const uint32_t sv = sk + kKVBytes;
+            const uint32_t sq = sv + kKVBytes;
+            // MMA1 needs the S^T accumulator released by the softmax warps
+            mbar_wait(&S.s_free, (it & 1u) ^ 1u);
+            tc_fence_after();
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < kD / 16; ++k) {
+                    const uint32_t koff = (k >> 2) * kHalf + (k & 3) * 32;
+                    const uint32_t qoff = (k >> 2) * (kN * 128) + (k & 3) * 32;
+                    mma_bf16(tmem_s, sdesc(sk + koff, 16, 1024), sdesc(sq + qoff, 16, 1024), id1, k > 0);
+                }
+                mma_commit(&S.s_full);
+            }
+            __syncwarp();
+            // MMA2 needs P^T of this tile and the O^T accumulator released
+            mbar_wait(&S.p_full, it & 1u);
+            mbar_wait(&S.o_free, (it & 1u) ^ 1u);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t sp = smem_u32(S.p);
+#pragma unroll
+                for (int k = 0; k < kTile / 16; ++k) {
+                    const uint32_t voff = k * 2048;  // 16 token rows of 128 B
+                    const uint32_t poff = (k >> 2) * (kN * 128) + (k & 3) * 32;
+                    mma_bf16(tmem_o, sdesc(sv + voff, kHalf, 1024), sdesc(sp + poff, 16, 1024), id2, k > 0);
+                }
+                mma_commit(&S.o_full);
+                mma_commit(&S.empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    } else {
+        // ================================ softmax / epilogue (warps 2..5)
+        const int ew = warp & 3;              // TMEM lane quadrant this warp may access
+        const int row = ew * 32 + lane;       // token row of S^T, then d row of O^T
+        const uint32_t lane_addr = static_cast<uint32_t>(ew * 32) << 16;
+        const float sl2 = static_cast<float>(p.scale_log2);
+        const float kNegInf = -INFINITY;
+        float m[kN], l[kN], acc[kN];
+        int stage = 0;
+        uint32_t phase = 0;
+        float* recs = static_cast<float*>(p.records);
+        for (uint32_t it = 0;; ++it) {
+            mbar_wait(&S.full[stage], phase);
+            const StageMeta md = S.meta[stage];
+            if (md.item < 0) break;
+            if (md.flags & 1) {
+#pragma unroll
+                for (int h = 0; h < kN; ++h) {
+                    m[h] = kNegInf;
+                    l[h] = 0.f;
+                    acc[h] = 0.f;
+                }
+            }
+            // ---- S^T row of this thread's token
+            mbar_wait(&S.s_full, it & 1u);
+            tc_fence_after();
+            float s[kN];
+            tmem_ld16(tmem_s + lane_addr, s);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.s_free);
+            const int tok = md.tile0 + row;
+            const bool valid = tok >= md.tlo && tok < md.thi;
+            float tmax[kN];
+#pragma unroll
+            for (int h = 0; h < kN; ++h) {
+                s[h] = valid ? s[h] * sl2 : kNegInf;
+                float v = s[h];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                tmax[h] = v;
+            }
+            const int rb = it & 1u;
+            if (lane == 0)
+#pragma unroll
+                for (int h = 0; h < kN; ++h) S.red_max[rb][ew][h] = tmax[h];
+            named_bar_sync(1, 128);
+            float corr[kN];
+#pragma unroll
+            for (int h = 0; h < kN; ++h) {
+                float mx = fmaxf(fmaxf(S.red_max[rb][0][h], S.red_max[rb][1][h]),
+                                 fmaxf(S.red_max[rb][2][h], S.red_max[rb][3][h]));
+                mx = fmaxf(mx, m[h]);
+                corr[h] = (mx == m[h]) ? 1.f : fast_exp2(m[h] - mx);
+                m[h] = mx;
+            }
+            // ---- P^T (bf16, swizzled K-major) and the running sums
+#pragma unroll
+            for (int h = 0; h < kN; ++h) {
+                const float pv = (valid && h < G) ? fast_exp2(s[h] - m[h]) : 0.f;
+                const bf16_t pb = Elem<bf16_t>::from_acc(pv);
+                l[h] = l[h] * corr[h] + Elem<bf16_t>::to_acc(pb);
+                if (h < G) *reinterpret_cast<uint16_t*>(S.p + swz_off(h, row, kN)) = pb.bits;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.p_full);
+            // ---- O^T row (d = row) of this tile
+            mbar_wait(&S.o_full, it & 1u);
+            tc_fence_after();
+            float o[kN];
+            tmem_ld16(tmem_o + lane_addr, o);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.o_free);
+#pragma unroll
+            for (int h = 0; h < kN; ++h) acc[h] = acc[h] * corr[h] + o[h];
+            if (md.flags & 2) {
+                // ---- finalize: e = sum over the 128 token rows of l
+                float tot[kN];
+#pragma unroll
+                for (int h = 0; h < kN; ++h) {
+                    float v = l[h];
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    tot[h] = v;
+                }
+                if (lane == 0)
+#pragma unroll
+                    for (int h = 0; h < kN; ++h) S.red_sum[ew][h] = tot[h];
+                named_bar_sync(1, 128);
+                const int64_t rec0 = static_cast<int64_t>(md.gchunk) * p.num_q_heads +
+                                     static_cast<int64_t>(md.kvh) * G;
+#pragma unroll
+                for (int h = 0; h < kN; ++h) {
+                    if (h >= G) continue;
+                    float* rec = recs + (rec0 + h) * (kD + 4);
+                    rec[4 + row] = acc[h];
+                    if (row == 0) {
+                        rec[0] = m[h] * 0.6931471805599453f;
+                        rec[1] = (S.red_sum[0][h] + S.red_sum[1][h]) + (S.red_sum[2][h] + S.red_sum[3][h]);
+                        rec[2] = static_cast<float>(md.thi - md.tlo);
+                        rec[3] = 0.f;
+                    }
+                }
+                named_bar_sync(1, 128);
+            }
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+}  // namespace tc
+
+size_t gqa_tc_smem_bytes() { return sizeof(tc::Smem) + 1024; }
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 2-D bf16 view [rows][128] with a (64 x box_rows) box and the 128-B swizzle.
+cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t dims[2] = {128, rows};
+    cuuint64_t strides[1] = {128 * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t gqa_tc_configure() {
+    return cudaFuncSetAttribute(reinterpret_cast<const void*>(&tc::gqa_tc_kernel),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(gqa_tc_smem_bytes()));
+}
+
+cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const MAParams& p,
+                          int grid, cudaStream_t st) {
+    const CUtensorMap* k = static_cast<const CUtensorMap*>(tm_k);
+    const CUtensorMap* v = static_cast<const CUtensorMap*>(tm_v);
+    const CUtensorMap* q = static_cast<const CUtensorMap*>(tm_q);
+    tc::gqa_tc_kernel<<<grid, tc::kThreads, gqa_tc_smem_bytes(), st>>>(*k, *v, *q, p);
+    return cudaGetLastError();
+}
+
+}  // namespace dattn

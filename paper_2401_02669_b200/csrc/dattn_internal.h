@@ -108,6 +108,12 @@ cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t 
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);
 cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
 cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
+// K2 (tcgen05 GQA path, dattn_gqa_tc.cu)
+size_t gqa_tc_smem_bytes();
+cudaError_t gqa_tc_configure();
+cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, uint32_t box_rows);
+cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const MAParams& p,
+                          int grid, cudaStream_t st);
 cudaError_t launch_identity_records(int dtype, int dp, void* recs, int64_t n, cudaStream_t st);
 
 }  // namespace dattn

@@ -464,15 +464,28 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
 }
 
 // ------------------------------------------------------------------ K3
+// One CTA (8 warps) per (row, q head) group. Pass 1: block max over live
+// records. Pass 2: warp w folds records w, w+8, ... with vector loads (each
+// lane owns kVW contiguous elements of ma), then the 8 warp partials are
+// summed through shared memory in a fixed order (deterministic).
+constexpr int kMergeWarps = 8;
+
 template <typename T, int DP>
-__global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergeParams p) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
     constexpr int REC = DP + 4;
-    constexpr int EPL = (DP + 31) / 32;
-    const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (g >= static_cast<int64_t>(p.rows) * p.heads) return;
+    constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
+                                           : (DP % 64 == 0 ? 2 : 1);
+    constexpr int kPer = 32 * kVW;                       // elements covered per lane sweep
+    constexpr int kSweeps = (DP + kPer - 1) / kPer;
+    __shared__ Acc s_max[kMergeWarps];
+    __shared__ Acc s_e[kMergeWarps];
+    __shared__ Acc s_tok[kMergeWarps];
+    __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
+
+    const int64_t g = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = static_cast<int>(g / p.heads);
     const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
     int n;
@@ -489,64 +502,93 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams p) {
     const int my_kvh = p.chunk_kvh ? h / p.group : 0;
     const Acc* R = static_cast<const Acc*>(p.recs);
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
-
-    Acc mg = kNegInf;
-    for (int c = lane; c < n; c += 32) {
+    auto live = [&](int c, const Acc* r) {
         if (p.chunk_kvh) {
             const int tag = p.chunk_kvh[cbase + c];
-            if (tag >= 0 && tag != my_kvh) continue;
+            if (tag >= 0 && tag != my_kvh) return false;
         }
+        return r[2] != Acc(0);  // identity (seq_p == 0) records are skipped
+    };
+
+    Acc mg = kNegInf;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
         const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
-        if (r[2] != Acc(0)) mg = r[0] > mg ? r[0] : mg;  // live (tokens > 0) records only
+        if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
         mg = o > mg ? o : mg;
     }
-    Acc eg = 0, ntok = 0;
-    Acc acc[EPL];
+    if (lane == 0) s_max[warp] = mg;
+    __syncthreads();
+    mg = s_max[0];
 #pragma unroll
-    for (int k = 0; k < EPL; ++k) acc[k] = 0;
-    for (int c = 0; c < n; ++c) {
-        if (p.chunk_kvh) {
-            const int tag = p.chunk_kvh[cbase + c];
-            if (tag >= 0 && tag != my_kvh) continue;
-        }
+    for (int w = 1; w < kMergeWarps; ++w) mg = s_max[w] > mg ? s_max[w] : mg;
+
+    Acc eg = 0, ntok = 0;
+    Acc acc[kSweeps][kVW];
+#pragma unroll
+    for (int s = 0; s < kSweeps; ++s)
+#pragma unroll
+        for (int v = 0; v < kVW; ++v) acc[s][v] = 0;
+    for (int c = warp; c < n; c += kMergeWarps) {
         const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
-        if (r[2] == Acc(0)) continue;  // identity (seq_p == 0): skipped, never rescaled
-        const Acc ec = r[1];
+        if (!live(c, r)) continue;
         const Acc mc = r[0];
         const Acc w = (mc == mg) ? Acc(1) : exp(mc - mg);
-        eg += ec * w;
+        eg += r[1] * w;
         ntok += r[2];
 #pragma unroll
-        for (int k = 0; k < EPL; ++k) {
-            const int j = lane + 32 * k;
-            if (j < DP) acc[k] += r[4 + j] * w;
+        for (int s = 0; s < kSweeps; ++s) {
+            const int j = s * kPer + lane * kVW;
+            if (j < DP) {
+                if constexpr (kVW == 4) {
+                    const float4 x = *reinterpret_cast<const float4*>(r + 4 + j);
+                    acc[s][0] += x.x * w; acc[s][1] += x.y * w; acc[s][2] += x.z * w; acc[s][3] += x.w * w;
+                } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
+                    const double2 x = *reinterpret_cast<const double2*>(r + 4 + j);
+                    acc[s][0] += x.x * w; acc[s][1] += x.y * w;
+                } else {
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) acc[s][v] += r[4 + j + v] * w;
+                }
+            }
         }
     }
-    if (p.out_recs) {
+#pragma unroll
+    for (int s = 0; s < kSweeps; ++s) {
+        const int j = s * kPer + lane * kVW;
+        if (j < DP)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) s_acc[warp][j + v] = acc[s][v];
+    }
+    if (lane == 0) {
+        s_e[warp] = eg;
+        s_tok[warp] = ntok;
+    }
+    __syncthreads();
+    Acc e_tot = 0, tok_tot = 0;
+#pragma unroll
+    for (int w = 0; w < kMergeWarps; ++w) {
+        e_tot += s_e[w];
+        tok_tot += s_tok[w];
+    }
+    for (int j = threadIdx.x; j < DP; j += blockDim.x) {
+        Acc a = 0;
+#pragma unroll
+        for (int w = 0; w < kMergeWarps; ++w) a += s_acc[w][j];
+        if (p.out_recs) static_cast<Acc*>(p.out_recs)[g * REC + 4 + j] = a;
+        if (p.out_norm)
+            static_cast<T*>(p.out_norm)[g * DP + j] =
+                E::from_acc(tok_tot != Acc(0) ? a / e_tot : Acc(0));
+    }
+    if (p.out_recs && threadIdx.x == 0) {
         Acc* o = static_cast<Acc*>(p.out_recs) + g * REC;
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) {
-            const int j = lane + 32 * k;
-            if (j < DP) o[4 + j] = acc[k];
-        }
-        if (lane == 0) {
-            o[0] = ntok != Acc(0) ? mg : kNegInf;
-            o[1] = eg;
-            o[2] = ntok;
-            o[3] = 0;
-        }
-    }
-    if (p.out_norm) {
-        T* o = static_cast<T*>(p.out_norm) + g * DP;
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) {
-            const int j = lane + 32 * k;
-            if (j < DP) o[j] = E::from_acc(ntok != Acc(0) ? acc[k] / eg : Acc(0));
-        }
+        o[0] = tok_tot != Acc(0) ? mg : kNegInf;
+        o[1] = e_tot;
+        o[2] = tok_tot;
+        o[3] = 0;
     }
 }
 
@@ -753,8 +795,8 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st) {
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     if (groups == 0) return cudaSuccess;
-    const int grid = static_cast<int>((groups + 7) / 8);
-    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    const int grid = static_cast<int>(groups);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
     return cudaGetLastError();
 }
 

@@ -198,6 +198,45 @@ def test_config3_gqa_shape(torch_cuda):
     assert rel_errs(out, ref) < 2e-2
 
 
+@pytest.mark.parametrize("group,lens", [(8, [4096, 129, 1, 2000]), (4, [700, 3333]), (16, [1500]),
+                                        (2, [257, 64])])
+def test_gqa_tcgen05_path_vs_oracle_and_cuda_core_path(torch_cuda, group, lens):
+    """K2 (tcgen05, swap-AB tiles) against the oracle and against K1 (CUDA
+    cores) on the same store, incl. rBlocks starting mid-page and per-kv-head
+    ranges."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    hkv = 4 if group <= 8 else 2
+    hq = hkv * group
+    st, seqs, q = make(torch, lens, hq, hkv, 128, pb.BF16, seed=group, amp_k=5.0)
+    rg = []
+    for b, (s, L) in enumerate(zip(seqs, lens)):
+        cut = min(L, 37)  # mid-page rBlock boundary
+        rg += [pb.Range(s, b, 0, cut), pb.Range(s, b, cut, L)]
+    out = decode(torch, st, rg, len(lens), q)
+    assert st.stats().last_kernel == 2
+    ref = oracle.decode_ranges(group, [0] * len(lens), lens, list(range(len(lens))), hq, hkv, 128,
+                               dtype=pb.BF16, amp_k=5.0)
+    got = out_np(torch, out, 128)
+    assert rel_errs(got, ref) < 2e-2
+    os.environ["DATTN_DISABLE_TC"] = "1"
+    try:
+        st1, seqs1, q1 = make(torch, lens, hq, hkv, 128, pb.BF16, seed=group, amp_k=5.0)
+    finally:
+        del os.environ["DATTN_DISABLE_TC"]
+    out1 = out_np(torch, decode(torch, st1, [pb.Range(seqs1[b], b, 0, L) for b, L in enumerate(lens)],
+                                len(lens), q1), 128)
+    assert st1.stats().last_kernel == 1
+    assert rel_errs(out1, ref) < 2e-2
+    # K2 rounds P to bf16 before the P.V MMA; both stay well inside the bf16 budget
+    assert rel_errs(got, out1) < 1e-2
+    # per-kv-head ranges (distattention.cpp:183-209) on the tcgen05 path
+    rk = [pb.Range(seqs[0], 0, 0, lens[0], kv_head=k) for k in range(hkv)]
+    outk = out_np(torch, decode(torch, st, rk, len(lens), q), 128)
+    assert rel_errs(outk[:1], ref[:1]) < 2e-2
+
+
 def test_adversarial_logits_and_partition_invariance(torch_cuda):
     """Key amplitude 30 (verify.cpp:90) forces large max shifts across chunks;
     any chunking / rBlock cut gives the same output."""
