@@ -135,9 +135,11 @@ def test_micro_attention_partials(torch_cuda, dtype):
                 assert rec[0] == -np.inf and rec[1] == 0 and not rec[4:].any()
                 continue
             tol = 1e-12 if dtype == 2 else 2e-5
+            # bf16 stores with a q group run K2, which rounds p to bf16 before P.V
+            tol_e = 4e-3 if dtype == 0 else tol
             assert abs(rec[0] - m) <= tol * max(1, abs(m))
-            assert abs(rec[1] - e) <= tol * e
-            assert np.abs(rec[4:4 + d] - ma).max() <= tol * np.abs(ma).max()
+            assert abs(rec[1] - e) <= tol_e * e
+            assert np.abs(rec[4:4 + d] - ma).max() <= tol_e * np.abs(ma).max()
 
 
 # ------------------------------------------------------------- decode paths
