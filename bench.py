@@ -317,6 +317,8 @@ def run_b200_arm(args, rank, ws, local):
     st.set_timing(False)
     ma_ms = s.ma_ms / max(s.ma_timed, 1)
     merge_ms = s.merge_ms / max(s.merge_timed, 1)
+    comm_ms = s.comm_ms / max(s.comm_timed, 1) if s.comm_timed else None
+    kernel_name = {1: "ma_decode_kernel (K1, CUDA cores)", 2: "gqa_tc_kernel (K2, tcgen05)"}.get(s.last_kernel, "?")
 
     # ---- region C: end to end through the C ABI with host buffers ----
     qh = q.cpu().pin_memory()
@@ -365,7 +367,7 @@ def run_b200_arm(args, rank, ws, local):
         "kv_gbs": w.kv_bytes() / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "ma_decode_kernel (K1)", "kernel_ms": ma_ms, "merge_ms": merge_ms,
+                     "kernel": kernel_name, "kernel_ms": ma_ms, "merge_ms": merge_ms, "allgather_ms": comm_ms,
                      "alg_bytes_per_launch": alg_rank, "peak_source": peak_src},
         "e2e": {"value": w.batch / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": qbytes + plan_bytes,
                 "d2h_bytes_per_step": qbytes, "ms_per_step": t_e2e * 1e3},

@@ -114,6 +114,8 @@ typedef struct dattn_stats {
     int32_t last_chunk_tokens, ma_grid;
     int32_t last_kernel;        /* 1: K1 CUDA-core MA, 2: K2 tcgen05 GQA MA */
     int32_t reserved;
+    int64_t comm_timed;
+    double comm_ms;             /* summed device time of timed ncclAllGather calls */
 } dattn_stats;
 dattn_status dattn_store_set_timing(dattn_store* s, int enable);
 dattn_status dattn_store_get_stats(dattn_store* s, int reset, dattn_stats* out);

@@ -93,6 +93,7 @@ class Stats(ctypes.Structure):
         ("last_items", ctypes.c_int64), ("last_chunks", ctypes.c_int64),
         ("last_plan_bytes", ctypes.c_int64), ("last_chunk_tokens", ctypes.c_int32),
         ("ma_grid", ctypes.c_int32), ("last_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("comm_timed", ctypes.c_int64), ("comm_ms", ctypes.c_double),
     ]
 
 

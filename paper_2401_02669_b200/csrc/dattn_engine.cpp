@@ -80,7 +80,7 @@ int elem_bytes_for(int dtype) { return dtype == kBF16 ? 2 : (dtype == kF32 ? 4 :
 
 dattn_store::~dattn_store() {
     if (comm) ncclCommDestroy(comm);
-    for (auto* v : {&ma_events, &merge_events})
+    for (auto* v : {&ma_events, &merge_events, &comm_events})
         for (auto& pr : *v) {
             cudaEventDestroy(pr[0]);
             cudaEventDestroy(pr[1]);
@@ -141,6 +141,7 @@ void dattn_store::init(const dattn_store_config& c) {
     cuda_check(cudaMalloc(&d_bt, bt), "cudaMalloc(block tables)");
     cuda_check(cudaMemsetAsync(d_bt, 0, bt, stream), "cudaMemset");
     cuda_check(cudaMalloc(&d_counter, 64), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(d_counter, 0, 64, stream), "cudaMemset");
     cuda_check(cudaMalloc(&d_flag, 64), "cudaMalloc");
     h_bt.assign(static_cast<size_t>(c.max_seqs) * c.max_pages_per_seq, 0);
     seq_tokens.assign(c.max_seqs, 0);
@@ -346,10 +347,10 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     const double s = scale > 0.0 ? scale : effective_scale();
     p.scale_log2 = s * 1.4426950408889634074;
     p.records = recs;
-    p.work_counter = d_counter;
+    p.work_counter = reinterpret_cast<unsigned long long*>(d_counter);
+    p.work_base = work_base;
     p.nonfinite_flag = check_finite ? d_flag : nullptr;
     p.stages = ma_stages;
-    cuda_check(cudaMemsetAsync(d_counter, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
     const bool use_tc = tc_ok && !check_finite;
     int grid;
     if (use_tc) {
@@ -371,6 +372,9 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     else
         cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+    // every CTA's producer claims items until one past the end: the counter
+    // advances by exactly nitems + grid per launch
+    work_base += static_cast<unsigned long long>(pl.nitems) + static_cast<unsigned long long>(grid);
     count_launch(1);
     stats.ma_launches++;
     stats.last_items = pl.nitems;
@@ -396,8 +400,8 @@ void dattn_store::run_merge(const MergeParams& mp) {
 // Event pairs around every MA (kind 0) / merge (kind 1) launch while timing
 // is on; summed by dattn_store_get_stats.
 cudaEvent_t* dattn_store::timer_pair(int kind) {
-    auto& v = kind == 0 ? ma_events : merge_events;
-    auto& used = kind == 0 ? ma_events_used : merge_events_used;
+    auto& v = kind == 0 ? ma_events : (kind == 1 ? merge_events : comm_events);
+    auto& used = kind == 0 ? ma_events_used : (kind == 1 ? merge_events_used : comm_events_used);
     if (used == v.size()) {
         std::array<cudaEvent_t, 2> pr{};
         cuda_check(cudaEventCreate(&pr[0]), "cudaEventCreate");
@@ -409,9 +413,9 @@ cudaEvent_t* dattn_store::timer_pair(int kind) {
 
 void dattn_store::collect_timing() {
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-    for (int kind = 0; kind < 2; ++kind) {
-        auto& v = kind == 0 ? ma_events : merge_events;
-        auto& used = kind == 0 ? ma_events_used : merge_events_used;
+    for (int kind = 0; kind < 3; ++kind) {
+        auto& v = kind == 0 ? ma_events : (kind == 1 ? merge_events : comm_events);
+        auto& used = kind == 0 ? ma_events_used : (kind == 1 ? merge_events_used : comm_events_used);
         double total = 0.0;
         for (size_t i = 0; i < used; ++i) {
             float ms = 0.f;
@@ -419,7 +423,8 @@ void dattn_store::collect_timing() {
             total += ms;
         }
         if (kind == 0) { stats.ma_ms += total; stats.ma_timed += used; }
-        else { stats.merge_ms += total; stats.merge_timed += used; }
+        else if (kind == 1) { stats.merge_ms += total; stats.merge_timed += used; }
+        else { stats.comm_ms += total; stats.comm_timed += used; }
         used = 0;
     }
 }
@@ -522,9 +527,12 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
     rowrecs.ensure(std::max<size_t>(row_recs, 1) * rec_bytes());
     local_merge(pl, recs.p, rowrecs.p, nullptr);
     gathered.ensure(std::max<size_t>(row_recs, 1) * rec_bytes() * nranks);
+    cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
+    if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
     nccl_check(ncclAllGather(rowrecs.p, gathered.p, row_recs * rec_elems,
                              cfg.dtype == kF64 ? ncclDouble : ncclFloat32, comm, stream),
                "ncclAllGather(partials)");
+    if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
     MergeParams mp{};
     mp.recs = gathered.p;
     mp.rows = b.num_rows;

@@ -84,6 +84,7 @@ struct dattn_store {
     dattn::DevBuf d_meta, recs, rowrecs, qbuf, obuf, gathered, d_staging;
     dattn::HostBuf h_meta, h_staging;
     size_t staging_used = 0;
+    unsigned long long work_base = 0;
     dattn::Plan scratch_plan;
 
     ncclComm_t comm = nullptr;
@@ -97,8 +98,8 @@ struct dattn_store {
 
     bool timing = false;
     dattn_stats stats{};
-    std::vector<std::array<cudaEvent_t, 2>> ma_events, merge_events;
-    size_t ma_events_used = 0, merge_events_used = 0;
+    std::vector<std::array<cudaEvent_t, 2>> ma_events, merge_events, comm_events;
+    size_t ma_events_used = 0, merge_events_used = 0, comm_events_used = 0;
     cudaEvent_t* timer_pair(int kind);
     void collect_timing();
 

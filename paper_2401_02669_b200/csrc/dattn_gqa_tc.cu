@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (;;) {
-                const int item = atomicAdd(p.work_counter, 1);
+                const int item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
                 if (item >= p.nitems) break;
                 const int r = find_item_range(p.item_prefix, p.nranges, item);
                 const RangeDev rg = p.ranges[r];

@@ -35,7 +35,8 @@ struct MAParams {
     int32_t chunk_tokens;
     double scale_log2;  // scale * log2(e)
     void* records;      // [chunks][Hq][DP+4] accumulation type
-    int32_t* work_counter;
+    unsigned long long* work_counter;  // monotonic across launches (no per-launch reset)
+    unsigned long long work_base;      // counter value at this launch's start
     int32_t* nonfinite_flag;  // may be null
     int32_t stages;
 };

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
         uint32_t phase = 0;
         for (;;) {
             int item = 0;
-            if (lane == 0) item = atomicAdd(p.work_counter, 1);
+            if (lane == 0) item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
             item = __shfl_sync(0xffffffffu, item, 0);
             if (item >= p.nitems) break;
             const int r = find_range(p.item_prefix, p.nranges, item);
