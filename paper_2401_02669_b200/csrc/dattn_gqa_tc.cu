@@ -40,8 +40,8 @@ constexpr int kHalf = kTile * 128;        // bytes of one 64-column half of a 12
 constexpr int kKVBytes = 2 * kHalf;       // one tensor (K or V) tile: 32 KB
 constexpr int kQBytes = 2 * kN * 128;     // Q slot: two halves of 16 rows x 128 B
 constexpr int kStageBytes = 2 * kKVBytes + kQBytes;  // K, V, Q = 68 KB
-constexpr int kPBytes = 2 * kN * 128;     // P^T tile
-constexpr uint32_t kTmemCols = 32;        // S^T cols 0..15, O^T cols 16..31
+constexpr int kPBytes = 2 * kN * 128;     // one P^T tile (two are kept)
+constexpr uint32_t kTmemCols = 64;        // S^T cols 0..15, O^T buffers at 16 and 32
 
 struct StageMeta {
     int32_t item;
@@ -53,9 +53,10 @@ struct StageMeta {
 
 struct Smem {
     uint8_t stage[kStages][kStageBytes];  // 1024-B aligned (offset 0)
-    uint8_t p[kPBytes];
+    uint8_t p[2][kPBytes];
     uint64_t full[kStages], empty[kStages];
-    uint64_t s_full, s_free, p_full, o_full, o_free;
+    uint64_t s_full, s_free;
+    uint64_t p_full[2], o_full[2], o_free[2];
     StageMeta meta[kStages];
     float red_max[2][4][kN];
     float red_sum[4][kN];
@@ -115,19 +116,6 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -150,12 +138,52 @@ __device__ __forceinline__ uint32_t swz_off(int row, int col, int rows) {
                                  ((c ^ (row & 7)) << 4) + ((col & 7) << 1));
 }
 
+// order-preserving float <-> int map so a warp max is one REDUX instruction
+__device__ __forceinline__ int f2ord(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+template <int NC>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[NC]) {
+    uint32_t r[NC];
+    if constexpr (NC == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+              "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    } else if constexpr (NC == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                       "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    } else if constexpr (NC == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr));
+    } else {
+        static_assert(NC == 2, "unsupported column count");
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                     : "=r"(r[0]), "=r"(r[1])
+                     : "r"(taddr));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < NC; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// GI: compile-time bound on the q group (2, 4, 8, 16); p.group <= GI, extra
+// heads are zero rows of Q and their columns are never written out.
+template <int GI>
 __global__ void __launch_bounds__(kThreads, 1)
     gqa_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                   const __grid_constant__ CUtensorMap tm_q, const MAParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // the swizzle pattern is tied to 1024-B address alignment
-    Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.group;
 
@@ -165,15 +193,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&S.empty[s], 1);
         }
         mbar_init(&S.s_full, 1);
-        mbar_init(&S.o_full, 1);
         mbar_init(&S.s_free, 4);
-        mbar_init(&S.p_full, 4);
-        mbar_init(&S.o_free, 4);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&S.o_full[b], 1);
+            mbar_init(&S.p_full[b], 4);
+            mbar_init(&S.o_free[b], 4);
+        }
         fence_mbar_init();
     }
     // zero the operand buffers once: padded Q / P rows must be 0 and stale
     // rows of partially filled tiles must be finite
-    for (int i = threadIdx.x; i < (kStages * kStageBytes + kPBytes) / 16; i += kThreads)
+    for (int i = threadIdx.x; i < (kStages * kStageBytes + 2 * kPBytes) / 16; i += kThreads)
         reinterpret_cast<uint4*>(S.stage)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -192,7 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
-    const uint32_t tmem_s = tmem, tmem_o = tmem + kN;
+    const uint32_t tmem_s = tmem;
+    const uint32_t tmem_o0 = tmem + kN;  // O^T of even tiles; odd tiles at + kN
 
     if (warp == 0) {
         // ================================ TMA producer
@@ -261,18 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ================================ MMA issuer
+        // Order: MMA1 of tile it+1 is issued before MMA2 of tile it, so the
+        // softmax warps find S^T(it+1) ready as soon as they hand over P(it).
         const uint32_t id1 = idesc(0), id2 = idesc(1);
-        int stage = 0;
-        uint32_t phase = 0;
-        for (uint32_t it = 0;; ++it) {
-            mbar_wait(&S.full[stage], phase);
-            const int item = S.meta[stage].item;
-            if (item < 0) break;
-            const uint32_t sk = smem_u32(S.stage[stage]);
-            const uint32_t sv = sk + kKVBytes;
-            const uint32_t sq = sv + kKVBytes;
-            // MMA1 needs the S^T accumulator released by the softmax warps
-            mbar_wait(&S.s_free, (it & 1u) ^ 1u);
+        auto issue_s = [&](int st) {
+            const uint32_t sk = smem_u32(S.stage[st]);
+            const uint32_t sq = sk + 2 * kKVBytes;
             tc_fence_after();
             if (lane == 0) {
 #pragma unroll
@@ -284,25 +309,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_commit(&S.s_full);
             }
             __syncwarp();
-            // MMA2 needs P^T of this tile and the O^T accumulator released
-            mbar_wait(&S.p_full, it & 1u);
-            mbar_wait(&S.o_free, (it & 1u) ^ 1u);
-            tc_fence_after();
-            if (lane == 0) {
-                const uint32_t sp = smem_u32(S.p);
-#pragma unroll
-                for (int k = 0; k < kTile / 16; ++k) {
-                    const uint32_t voff = k * 2048;  // 16 token rows of 128 B
-                    const uint32_t poff = (k >> 2) * (kN * 128) + (k & 3) * 32;
-                    mma_bf16(tmem_o, sdesc(sv + voff, kHalf, 1024), sdesc(sp + poff, 16, 1024), id2, k > 0);
+        };
+        int stage = 0;
+        uint32_t phase = 0;
+        mbar_wait(&S.full[0], 0);
+        if (S.meta[0].item >= 0) {
+            issue_s(0);
+            for (uint32_t it = 0;; ++it) {
+                int nst = stage + 1;
+                uint32_t nph = phase;
+                if (nst == kStages) {
+                    nst = 0;
+                    nph ^= 1u;
                 }
-                mma_commit(&S.o_full);
-                mma_commit(&S.empty[stage]);
-            }
-            __syncwarp();
-            if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1u;
+                mbar_wait(&S.full[nst], nph);
+                const bool more = S.meta[nst].item >= 0;
+                if (more) {
+                    mbar_wait(&S.s_free, it & 1u);  // softmax warps hold S^T(it) in registers
+                    issue_s(nst);
+                }
+                // MMA2 of tile it: needs P^T(it) and its O^T buffer released
+                const uint32_t ob = it & 1u, oph = (it >> 1) & 1u;
+                mbar_wait(&S.p_full[ob], oph);
+                mbar_wait(&S.o_free[ob], oph ^ 1u);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sv = smem_u32(S.stage[stage]) + kKVBytes;
+                    const uint32_t sp = smem_u32(S.p[ob]);
+#pragma unroll
+                    for (int k = 0; k < kTile / 16; ++k) {
+                        const uint32_t voff = k * 2048;  // 16 token rows of 128 B
+                        const uint32_t poff = (k >> 2) * (kN * 128) + (k & 3) * 32;
+                        mma_bf16(tmem_o0 + ob * kN, sdesc(sv + voff, kHalf, 1024), sdesc(sp + poff, 16, 1024),
+                                 id2, k > 0);
+                    }
+                    mma_commit(&S.o_full[ob]);
+                    mma_commit(&S.empty[stage]);
+                }
+                __syncwarp();
+                if (!more) break;
+                stage = nst;
+                phase = nph;
             }
         }
     } else {
@@ -312,7 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = static_cast<uint32_t>(ew * 32) << 16;
         const float sl2 = static_cast<float>(p.scale_log2);
         const float kNegInf = -INFINITY;
-        float m[kN], l[kN], acc[kN];
+        float m[GI], l[GI], acc[GI], corr_prev[GI];
+        bool pending = false;  // an O^T tile of the current item not yet accumulated
         int stage = 0;
         uint32_t phase = 0;
         float* recs = static_cast<float*>(p.records);
@@ -322,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (md.item < 0) break;
             if (md.flags & 1) {
 #pragma unroll
-                for (int h = 0; h < kN; ++h) {
+                for (int h = 0; h < GI; ++h) {
                     m[h] = kNegInf;
                     l[h] = 0.f;
                     acc[h] = 0.f;
@@ -331,75 +379,84 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ---- S^T row of this thread's token
             mbar_wait(&S.s_full, it & 1u);
             tc_fence_after();
-            float s[kN];
-            tmem_ld16(tmem_s + lane_addr, s);
+            float s[GI];
+            tmem_ld<GI>(tmem_s + lane_addr, s);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.s_free);
             const int tok = md.tile0 + row;
             const bool valid = tok >= md.tlo && tok < md.thi;
-            float tmax[kN];
-#pragma unroll
-            for (int h = 0; h < kN; ++h) {
-                s[h] = valid ? s[h] * sl2 : kNegInf;
-                float v = s[h];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-                tmax[h] = v;
-            }
             const int rb = it & 1u;
-            if (lane == 0)
 #pragma unroll
-                for (int h = 0; h < kN; ++h) S.red_max[rb][ew][h] = tmax[h];
+            for (int h = 0; h < GI; ++h) {
+                s[h] = valid ? s[h] * sl2 : kNegInf;
+                const int wmax = __reduce_max_sync(0xffffffffu, f2ord(s[h]));
+                if (lane == 0) S.red_max[rb][ew][h] = ord2f(wmax);
+            }
             named_bar_sync(1, 128);
-            float corr[kN];
+            float corr[GI];
 #pragma unroll
-            for (int h = 0; h < kN; ++h) {
+            for (int h = 0; h < GI; ++h) {
                 float mx = fmaxf(fmaxf(S.red_max[rb][0][h], S.red_max[rb][1][h]),
                                  fmaxf(S.red_max[rb][2][h], S.red_max[rb][3][h]));
                 mx = fmaxf(mx, m[h]);
                 corr[h] = (mx == m[h]) ? 1.f : fast_exp2(m[h] - mx);
                 m[h] = mx;
             }
-            // ---- P^T (bf16, swizzled K-major) and the running sums
+            // ---- P^T (bf16, swizzled K-major) into buffer it&1, running sums
+            const uint32_t ob = it & 1u, oph = (it >> 1) & 1u;
 #pragma unroll
-            for (int h = 0; h < kN; ++h) {
-                const float pv = (valid && h < G) ? fast_exp2(s[h] - m[h]) : 0.f;
+            for (int h = 0; h < GI; ++h) {
+                const float pv = valid ? fast_exp2(s[h] - m[h]) : 0.f;
                 const bf16_t pb = Elem<bf16_t>::from_acc(pv);
                 l[h] = l[h] * corr[h] + Elem<bf16_t>::to_acc(pb);
-                if (h < G) *reinterpret_cast<uint16_t*>(S.p + swz_off(h, row, kN)) = pb.bits;
+                *reinterpret_cast<uint16_t*>(S.p[ob] + swz_off(h, row, kN)) = pb.bits;
             }
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.p_full);
-            // ---- O^T row (d = row) of this tile
-            mbar_wait(&S.o_full, it & 1u);
-            tc_fence_after();
-            float o[kN];
-            tmem_ld16(tmem_o + lane_addr, o);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.o_free);
+            if (lane == 0) mbar_arrive(&S.p_full[ob]);
+            // ---- O^T of the PREVIOUS tile (deferred so this tile's softmax did
+            //      not wait for its P.V round trip): acc = acc*corr_prev + O_prev
+            if (pending) {
+                const uint32_t pb_ = ob ^ 1u, pph = ((it - 1) >> 1) & 1u;
+                mbar_wait(&S.o_full[pb_], pph);
+                tc_fence_after();
+                float o[GI];
+                tmem_ld<GI>(tmem_o0 + pb_ * kN + lane_addr, o);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.o_free[pb_]);
 #pragma unroll
-            for (int h = 0; h < kN; ++h) acc[h] = acc[h] * corr[h] + o[h];
+                for (int h = 0; h < GI; ++h) acc[h] = acc[h] * corr_prev[h] + o[h];
+            }
+#pragma unroll
+            for (int h = 0; h < GI; ++h) corr_prev[h] = corr[h];
+            pending = true;
             if (md.flags & 2) {
-                // ---- finalize: e = sum over the 128 token rows of l
-                float tot[kN];
+                // ---- flush this tile's O^T, then finalize the item
+                mbar_wait(&S.o_full[ob], oph);
+                tc_fence_after();
+                float o[GI];
+                tmem_ld<GI>(tmem_o0 + ob * kN + lane_addr, o);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.o_free[ob]);
 #pragma unroll
-                for (int h = 0; h < kN; ++h) {
+                for (int h = 0; h < GI; ++h) acc[h] = acc[h] * corr[h] + o[h];
+                pending = false;
+                // e = sum over the 128 token rows of l
+#pragma unroll
+                for (int h = 0; h < GI; ++h) {
                     float v = l[h];
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                    tot[h] = v;
+                    if (lane == 0) S.red_sum[ew][h] = v;
                 }
-                if (lane == 0)
-#pragma unroll
-                    for (int h = 0; h < kN; ++h) S.red_sum[ew][h] = tot[h];
                 named_bar_sync(1, 128);
                 const int64_t rec0 = static_cast<int64_t>(md.gchunk) * p.num_q_heads +
                                      static_cast<int64_t>(md.kvh) * G;
 #pragma unroll
-                for (int h = 0; h < kN; ++h) {
+                for (int h = 0; h < GI; ++h) {
                     if (h >= G) continue;
                     float* rec = recs + (rec0 + h) * (kD + 4);
                     rec[4 + row] = acc[h];
@@ -458,10 +515,20 @@ cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, ui
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static const void* gqa_fn(int group) {
+    if (group <= 2) return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<2>);
+    if (group <= 4) return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<4>);
+    if (group <= 8) return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<8>);
+    return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<16>);
+}
+
 cudaError_t gqa_tc_configure() {
-    return cudaFuncSetAttribute(reinterpret_cast<const void*>(&tc::gqa_tc_kernel),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(gqa_tc_smem_bytes()));
+    for (int g : {2, 4, 8, 16}) {
+        const cudaError_t e = cudaFuncSetAttribute(gqa_fn(g), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(gqa_tc_smem_bytes()));
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const MAParams& p,
@@ -469,8 +536,9 @@ cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, 
     const CUtensorMap* k = static_cast<const CUtensorMap*>(tm_k);
     const CUtensorMap* v = static_cast<const CUtensorMap*>(tm_v);
     const CUtensorMap* q = static_cast<const CUtensorMap*>(tm_q);
-    tc::gqa_tc_kernel<<<grid, tc::kThreads, gqa_tc_smem_bytes(), st>>>(*k, *v, *q, p);
-    return cudaGetLastError();
+    MAParams pp = p;
+    void* args[] = {const_cast<CUtensorMap*>(k), const_cast<CUtensorMap*>(v), const_cast<CUtensorMap*>(q), &pp};
+    return cudaLaunchKernel(gqa_fn(p.group), dim3(grid), dim3(tc::kThreads), args, gqa_tc_smem_bytes(), st);
 }
 
 }  // namespace dattn
