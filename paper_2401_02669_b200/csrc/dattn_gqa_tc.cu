@@ -41,6 +41,7 @@ constexpr int kKVBytes = 2 * kHalf;       // one tensor (K or V) tile: 32 KB
 constexpr int kQBytes = 2 * kN * 128;     // Q slot: two halves of 16 rows x 128 B
 constexpr int kStageBytes = 2 * kKVBytes + kQBytes;  // K, V, Q = 68 KB
 constexpr int kPBytes = 2 * kN * 128;     // one P^T tile (two are kept)
+constexpr int kPidWin = 512;               // page ids of one item held in shared memory
 constexpr uint32_t kTmemCols = 64;        // S^T cols 0..15, O^T buffers at 16 and 32
 
 struct StageMeta {
@@ -58,6 +59,7 @@ struct Smem {
     uint64_t s_full, s_free;
     uint64_t p_full[2], o_full[2], o_free[2];
     StageMeta meta[kStages];
+    int32_t pid[kPidWin];
     float red_max[2][4][kN];
     float red_sum[4][kN];
     uint32_t tmem_base;
@@ -227,27 +229,42 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ================================ TMA producer
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            const int P = p.page_tokens;
-            int stage = 0;
-            uint32_t phase = 0;
-            for (;;) {
-                const int item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
-                if (item >= p.nitems) break;
-                const int r = find_item_range(p.item_prefix, p.nranges, item);
-                const RangeDev rg = p.ranges[r];
-                const int local = item - __ldg(p.item_prefix + r);
-                const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
-                const int j = local / nh;
-                const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
-                const int tlo = rg.lo + j * p.chunk_tokens;
-                const int thi = min(rg.hi, tlo + p.chunk_tokens);
-                const int gchunk = __ldg(p.chunk_prefix + r) + j;
-                const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
-                const int start = (tlo / P) * P;
-                const int qrow = rg.out_row * p.num_q_heads + kvh * G;
-                for (int t0 = start; t0 < thi; t0 += kTile) {
+        // The whole warp decodes each item and fetches its page ids into
+        // shared memory in one round trip; lane 0 then streams the tiles.
+        const uint64_t pol = l2_policy_evict_first();
+        const int P = p.page_tokens;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            int item = 0;
+            if (lane == 0) item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= p.nitems) break;
+            const int r = find_item_range(p.item_prefix, p.nranges, item);
+            const RangeDev rg = p.ranges[r];
+            const int local = item - __ldg(p.item_prefix + r);
+            const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
+            const int j = local / nh;
+            const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
+            const int tlo = rg.lo + j * p.chunk_tokens;
+            const int thi = min(rg.hi, tlo + p.chunk_tokens);
+            const int gchunk = __ldg(p.chunk_prefix + r) + j;
+            const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
+            const int start = (tlo / P) * P;
+            const int qrow = rg.out_row * p.num_q_heads + kvh * G;
+            const int pfirst = start / P, plast = (thi - 1) / P;
+            int win = -1;  // first page id held in S.pid
+            for (int t0 = start; t0 < thi; t0 += kTile) {
+                const int tend = min(thi, t0 + kTile);
+                const int pg0 = t0 / P, npages = (tend - 1) / P - pg0 + 1;
+                if (win < 0 || pg0 + npages > win + kPidWin) {
+                    __syncwarp();
+                    win = pg0;
+                    for (int i = lane; i < kPidWin; i += 32)
+                        if (win + i <= plast) S.pid[i] = __ldg(bt + win + i);
+                    __syncwarp();
+                }
+                if (lane == 0) {
                     mbar_wait(&S.empty[stage], phase ^ 1u);
                     StageMeta& md = S.meta[stage];
                     md.item = item;
@@ -258,20 +275,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     md.row = rg.out_row;
                     md.kvh = kvh;
                     md.gchunk = gchunk;
-                    const int tend = min(thi, t0 + kTile);
-                    const int npages = (tend - 1) / P - t0 / P + 1;
                     mbar_arrive_expect_tx(&S.full[stage],
                                           static_cast<uint32_t>(npages * P * 128 * 4 + G * 128 * 2));
                     uint8_t* sk = S.stage[stage];
                     uint8_t* sv = sk + kKVBytes;
                     uint8_t* sq = sv + kKVBytes;
-                    // independent block-table loads first (one round trip per tile)
-                    int pages[kTile / 16];
-#pragma unroll
-                    for (int pg = 0; pg < kTile / 16; ++pg)
-                        pages[pg] = pg < npages ? __ldg(bt + t0 / P + pg) : 0;
                     for (int pg = 0; pg < npages; ++pg) {
-                        const int row0 = (pages[pg] * p.num_kv_heads + kvh) * P;
+                        const int row0 = (S.pid[pg0 - win + pg] * p.num_kv_heads + kvh) * P;
                         const int off = pg * P * 128;
                         tma_load_2d(sk + off, &tm_k, 0, row0, &S.full[stage], pol);
                         tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.full[stage], pol);
@@ -280,12 +290,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tma_load_2d(sq, &tm_q, 0, qrow, &S.full[stage], 0);
                     tma_load_2d(sq + kN * 128, &tm_q, 64, qrow, &S.full[stage], 0);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+                }
+                __syncwarp();
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
+            (void)pfirst;
+        }
+        if (lane == 0) {
             mbar_wait(&S.empty[stage], phase ^ 1u);
             S.meta[stage].item = -1;
             mbar_arrive(&S.full[stage]);
