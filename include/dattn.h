@@ -113,9 +113,9 @@ typedef struct dattn_stats {
     int64_t last_items, last_chunks, last_plan_bytes;
     int32_t last_chunk_tokens, ma_grid;
     int32_t last_kernel;        /* 1: K1 CUDA-core MA, 2: K2 tcgen05 GQA MA */
-    int32_t reserved;
+    int32_t last_exchange;      /* 1: NCCL allgather + K3, 2: fused K5 NVLink exchange */
     int64_t comm_timed;
-    double comm_ms;             /* summed device time of timed ncclAllGather calls */
+    double comm_ms;             /* summed device time of the timed exchange (allgather or K5) */
 } dattn_stats;
 dattn_status dattn_store_set_timing(dattn_store* s, int enable);
 dattn_status dattn_store_get_stats(dattn_store* s, int reset, dattn_stats* out);

@@ -70,7 +70,7 @@ class Range(ctypes.Structure):
     output row ``out_row`` (kv_head -1: every kv head)."""
     _fields_ = [
         ("seq", ctypes.c_int32), ("out_row", ctypes.c_int32), ("kv_head", ctypes.c_int32),
-        ("reserved", ctypes.c_int32), ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64),
+        ("last_exchange", ctypes.c_int32), ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64),
     ]
 
     def __init__(self, seq=0, out_row=0, tok_begin=0, tok_end=0, kv_head=-1):
@@ -92,7 +92,7 @@ class Stats(ctypes.Structure):
         ("ma_ms", ctypes.c_double), ("merge_ms", ctypes.c_double),
         ("last_items", ctypes.c_int64), ("last_chunks", ctypes.c_int64),
         ("last_plan_bytes", ctypes.c_int64), ("last_chunk_tokens", ctypes.c_int32),
-        ("ma_grid", ctypes.c_int32), ("last_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("ma_grid", ctypes.c_int32), ("last_kernel", ctypes.c_int32), ("last_exchange", ctypes.c_int32),
         ("comm_timed", ctypes.c_int64), ("comm_ms", ctypes.c_double),
     ]
 

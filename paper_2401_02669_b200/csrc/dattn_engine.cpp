@@ -78,7 +78,75 @@ int elem_bytes_for(int dtype) { return dtype == kBF16 ? 2 : (dtype == kF32 ? 4 :
 
 // ------------------------------------------------------------------ store
 
+void dattn_store::release_exchange() {
+    for (int r = 0; r < 8; ++r) {
+        if (r != rank && peer_x[r]) cudaIpcCloseMemHandle(peer_x[r]);
+        if (r != rank && peer_flags[r]) cudaIpcCloseMemHandle(peer_flags[r]);
+        peer_x[r] = nullptr;
+        peer_flags[r] = nullptr;
+    }
+    if (xbuf) cudaFree(xbuf);
+    if (xflags) cudaFree(xflags);
+    xbuf = nullptr;
+    xflags = nullptr;
+    fused_merge = false;
+}
+
+// Map every rank's exchange buffers into this process (CUDA IPC); the 64-byte
+// handles travel through the NCCL communicator itself.
+void dattn_store::setup_exchange() {
+    release_exchange();
+    const char* env = std::getenv("DATTN_FUSED_MERGE");
+    if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
+    slot_stride = static_cast<int64_t>(cfg.max_seqs) * cfg.num_q_heads;
+    const size_t xbytes = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
+    const size_t fbytes = static_cast<size_t>(nranks) * slot_stride * sizeof(uint32_t);
+    cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
+    cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
+    cudaIpcMemHandle_t hx, hf;
+    cuda_check(cudaIpcGetMemHandle(&hx, xbuf), "cudaIpcGetMemHandle");
+    cuda_check(cudaIpcGetMemHandle(&hf, xflags), "cudaIpcGetMemHandle");
+    constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+    std::vector<unsigned char> mine(2 * kH), all(2 * kH * nranks);
+    std::memcpy(mine.data(), &hx, kH);
+    std::memcpy(mine.data() + kH, &hf, kH);
+    DevBuf dh;
+    dh.ensure(all.size());
+    cuda_check(cudaMemcpyAsync(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, mine.data(), 2 * kH,
+                               cudaMemcpyHostToDevice, stream),
+               "cudaMemcpyAsync");
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, dh.p, 2 * kH, ncclUint8,
+                             comm, stream),
+               "ncclAllGather(ipc handles)");
+    cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) {
+            peer_x[r] = xbuf;
+            peer_flags[r] = xflags;
+            continue;
+        }
+        cudaIpcMemHandle_t px, pf;
+        std::memcpy(&px, all.data() + r * 2 * kH, kH);
+        std::memcpy(&pf, all.data() + r * 2 * kH + kH, kH);
+        cuda_check(cudaIpcOpenMemHandle(&peer_x[r], px, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        void* f = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&f, pf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        peer_flags[r] = static_cast<uint32_t*>(f);
+    }
+    // every rank has zeroed its flags before anyone can publish
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, dh.p, 2 * kH, ncclUint8,
+                             comm, stream),
+               "ncclAllGather(barrier)");
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    epoch = 0;
+    fused_merge = true;
+}
+
 dattn_store::~dattn_store() {
+    release_exchange();
     if (comm) ncclCommDestroy(comm);
     for (auto* v : {&ma_events, &merge_events, &comm_events})
         for (auto& pr : *v) {
@@ -524,6 +592,47 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
     recs.ensure(static_cast<size_t>(std::max(pl.nchunks, 1)) * cfg.num_q_heads * rec_bytes());
     run_ma(pl, q_dev, recs.p, b.scale, false);
     const size_t row_recs = static_cast<size_t>(b.num_rows) * cfg.num_q_heads;
+    void* out_dev0 = out;
+    if (mem == DATTN_MEM_HOST) {
+        obuf.ensure(q_bytes(b.num_rows));
+        out_dev0 = obuf.p;
+    }
+    if (fused_merge && static_cast<int64_t>(row_recs) <= slot_stride) {
+        // K5: local merge + NVLink record exchange + rank merge in one launch
+        const int32_t* w = static_cast<const int32_t*>(d_meta.p);
+        XParams xp{};
+        xp.local.recs = recs.p;
+        xp.local.rows = b.num_rows;
+        xp.local.heads = cfg.num_q_heads;
+        xp.local.row_begin = w + pl.off_rowchunk;
+        xp.local.row_mul = cfg.num_q_heads;
+        xp.local.c_stride = cfg.num_q_heads;
+        xp.local.chunk_kvh = pl.any_kvh ? w + pl.off_kvh : nullptr;
+        xp.local.group = group;
+        for (int r = 0; r < nranks; ++r) {
+            xp.peer_x[r] = peer_x[r];
+            xp.peer_flags[r] = peer_flags[r];
+        }
+        xp.rank = rank;
+        xp.nranks = nranks;
+        xp.slot_stride = slot_stride;
+        xp.epoch = ++epoch;
+        xp.out_norm = out_dev0;
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>(static_cast<int64_t>(row_recs), static_cast<int64_t>(num_sms) * 4)));
+        cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
+        if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
+        cuda_check(launch_merge_exchange(cfg.dtype, dp, xp, grid, stream), "launch(K5 merge_exchange)");
+        if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+        count_launch(1);
+        stats.last_exchange = 2;
+        if (mem == DATTN_MEM_HOST) {
+            cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost, stream),
+                       "cudaMemcpyAsync(out)");
+            cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+        }
+        return;
+    }
     rowrecs.ensure(std::max<size_t>(row_recs, 1) * rec_bytes());
     local_merge(pl, recs.p, rowrecs.p, nullptr);
     gathered.ensure(std::max<size_t>(row_recs, 1) * rec_bytes() * nranks);
@@ -533,6 +642,7 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
                              cfg.dtype == kF64 ? ncclDouble : ncclFloat32, comm, stream),
                "ncclAllGather(partials)");
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+    stats.last_exchange = 1;
     MergeParams mp{};
     mp.recs = gathered.p;
     mp.rows = b.num_rows;
@@ -897,6 +1007,7 @@ dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE
         nccl_check(ncclCommInitRank(&s->comm, nranks, u, rank), "ncclCommInitRank");
         s->rank = rank;
         s->nranks = nranks;
+        if (nranks > 1) s->setup_exchange();
     });
 }
 

@@ -89,6 +89,16 @@ struct dattn_store {
 
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
+    // K5 exchange: IPC-mapped record/flag buffers of every rank
+    void* xbuf = nullptr;        // own [nranks][slot_stride][rec]
+    uint32_t* xflags = nullptr;  // own [nranks][slot_stride]
+    void* peer_x[8]{};
+    uint32_t* peer_flags[8]{};
+    int64_t slot_stride = 0;
+    uint32_t epoch = 0;
+    bool fused_merge = false;
+    void setup_exchange();
+    void release_exchange();
 
     // K2 (tcgen05) path for grouped-query bf16 stores
     bool tc_ok = false;

@@ -56,6 +56,19 @@ struct MergeParams {
     void* out_norm;            // [rows*heads][DP] storage dtype, or null
 };
 
+// K5: fused local merge + NVLink exchange + rank merge (one launch per step).
+constexpr int kMaxRanks = 8;
+struct XParams {
+    MergeParams local;                 // chunk records of this rank (out_* unused)
+    void* peer_x[kMaxRanks];           // exchange buffers of every rank (own at [rank])
+    uint32_t* peer_flags[kMaxRanks];   // arrival flags of every rank
+    int32_t rank;
+    int32_t nranks;
+    int64_t slot_stride;               // records per source rank in an exchange buffer
+    uint32_t epoch;                    // this step's flag value
+    void* out_norm;                    // [rows*heads][DP] storage dtype
+};
+
 struct FillParams {
     void* k_pool;
     void* v_pool;
@@ -105,6 +118,7 @@ cudaError_t ma_occupancy(int dtype, int dp, int group, size_t smem, int* blocks_
 cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t smem,
                       cudaStream_t st);
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
+cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st);
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st);
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);
 cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st);

@@ -592,6 +592,168 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
     }
 }
 
+// ------------------------------------------------------------------ K5
+// Fused cross-GPU merge: a persistent grid walks the (row, q
+// head) groups in the same order on every rank. For each group it merges this
+// rank's chunk records (as K3), stores the merged record straight into every
+// rank's exchange buffer over NVLink (peer pointers from CUDA IPC), publishes
+// it with a release store of the step epoch into the owner's flag, waits for
+// the flags of all ranks (acquire, system scope) and merges the nranks records
+// into the output. Replaces local K3 + ncclAllGather + rank K3.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T, int DP>
+__global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const XParams x) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int REC = DP + 4;
+    __shared__ Acc s_max[kMergeWarps];
+    __shared__ Acc s_e[kMergeWarps];
+    __shared__ Acc s_tok[kMergeWarps];
+    __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
+    __shared__ __align__(16) Acc s_rec[REC];
+    const MergeParams& p = x.local;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
+    const Acc* R = static_cast<const Acc*>(p.recs);
+    for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+        // ---- 1. merge this rank's chunks of group g (K3 algorithm)
+        const int row = static_cast<int>(g / p.heads);
+        const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
+        const int cbase = p.row_begin[row];
+        const int n = p.row_begin[row + 1] - cbase;
+        const int64_t base = static_cast<int64_t>(cbase) * p.row_mul + h;
+        const int my_kvh = p.chunk_kvh ? h / p.group : 0;
+        auto live = [&](int c, const Acc* r) {
+            if (p.chunk_kvh) {
+                const int tag = p.chunk_kvh[cbase + c];
+                if (tag >= 0 && tag != my_kvh) return false;
+            }
+            return r[2] != Acc(0);
+        };
+        Acc mg = kNegInf;
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+            if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+            mg = o > mg ? o : mg;
+        }
+        if (lane == 0) s_max[warp] = mg;
+        __syncthreads();
+        mg = s_max[0];
+#pragma unroll
+        for (int w = 1; w < kMergeWarps; ++w) mg = s_max[w] > mg ? s_max[w] : mg;
+        Acc eg = 0, ntok = 0;
+        Acc acc[(DP + 31) / 32];
+#pragma unroll
+        for (int k = 0; k < (DP + 31) / 32; ++k) acc[k] = 0;
+        for (int c = warp; c < n; c += kMergeWarps) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+            if (!live(c, r)) continue;
+            const Acc w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
+            eg += r[1] * w;
+            ntok += r[2];
+#pragma unroll
+            for (int k = 0; k < (DP + 31) / 32; ++k) {
+                const int j = lane + 32 * k;
+                if (j < DP) acc[k] += r[4 + j] * w;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (DP + 31) / 32; ++k) {
+            const int j = lane + 32 * k;
+            if (j < DP) s_acc[warp][j] = acc[k];
+        }
+        if (lane == 0) {
+            s_e[warp] = eg;
+            s_tok[warp] = ntok;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < DP; j += blockDim.x) {
+            Acc a = 0;
+#pragma unroll
+            for (int w = 0; w < kMergeWarps; ++w) a += s_acc[w][j];
+            s_rec[4 + j] = a;
+        }
+        if (threadIdx.x == 0) {
+            Acc e_tot = 0, tok_tot = 0;
+#pragma unroll
+            for (int w = 0; w < kMergeWarps; ++w) {
+                e_tot += s_e[w];
+                tok_tot += s_tok[w];
+            }
+            s_rec[0] = tok_tot != Acc(0) ? mg : kNegInf;
+            s_rec[1] = e_tot;
+            s_rec[2] = tok_tot;
+            s_rec[3] = 0;
+        }
+        __syncthreads();
+        // ---- 2. push the record to every rank, then publish it
+        const int64_t slot = static_cast<int64_t>(x.rank) * x.slot_stride + g;
+        for (int r = 0; r < x.nranks; ++r) {
+            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot * REC;
+            for (int j = threadIdx.x; j < REC; j += blockDim.x) dst[j] = s_rec[j];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int r = 0; r < x.nranks; ++r) st_release_sys(x.peer_flags[r] + slot, x.epoch);
+        }
+        // ---- 3. wait for every rank's record of group g
+        if (threadIdx.x < x.nranks) {
+            const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(threadIdx.x) * x.slot_stride + g;
+            while (ld_acquire_sys(f) != x.epoch) {
+            }
+        }
+        __syncthreads();
+        // ---- 4. rank merge (records read past L1: they were written remotely)
+        const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
+        if (warp == 0) {
+            Acc m2 = kNegInf, e2 = 0;
+            Acc a2[(DP + 31) / 32];
+#pragma unroll
+            for (int k = 0; k < (DP + 31) / 32; ++k) a2[k] = 0;
+            for (int r = 0; r < x.nranks; ++r) {
+                const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+                if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
+            }
+            Acc tok2 = 0;
+            for (int r = 0; r < x.nranks; ++r) {
+                const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+                const Acc tk = __ldcv(rec + 2);
+                if (tk == Acc(0)) continue;
+                const Acc mr = __ldcv(rec);
+                const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
+                e2 += __ldcv(rec + 1) * w;
+                tok2 += tk;
+#pragma unroll
+                for (int k = 0; k < (DP + 31) / 32; ++k) {
+                    const int j = lane + 32 * k;
+                    if (j < DP) a2[k] += __ldcv(rec + 4 + j) * w;
+                }
+            }
+            T* o = static_cast<T*>(x.out_norm) + g * DP;
+#pragma unroll
+            for (int k = 0; k < (DP + 31) / 32; ++k) {
+                const int j = lane + 32 * k;
+                if (j < DP) o[j] = E::from_acc(tok2 != Acc(0) ? a2[k] / e2 : Acc(0));
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ K4
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -804,6 +966,11 @@ static int grid_for(int64_t total) {
     int64_t g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
     return static_cast<int>(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st) {
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_exchange_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st) {

@@ -32,7 +32,7 @@ CASES = {
 }
 
 
-def _worker(rank, world, port, case, placement, q):
+def _worker(rank, world, port, case, placement, fused, q):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -43,6 +43,7 @@ def _worker(rank, world, port, case, placement, q):
     from paper_2401_02669_b200.sharding import placement_from_moves, plan_rank_ranges
 
     try:
+        os.environ["DATTN_FUSED_MERGE"] = "1" if fused else "0"
         torch.cuda.set_device(rank)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -74,6 +75,11 @@ def _worker(rank, world, port, case, placement, q):
         st.comm_init(uid[0], rank, world)
         st.decode_sharded(ranges, len(lens), qd, out)
         torch.cuda.synchronize()
+        assert st.stats().last_exchange == (2 if fused else 1)
+        # repeated steps reuse the exchange buffers (epoch flags)
+        for _ in range(3):
+            st.decode_sharded(ranges, len(lens), qd, out)
+        torch.cuda.synchronize()
         # host-memory path gives the same bytes
         qh = qd.cpu().pin_memory()
         oh = torch.zeros_like(qh).pin_memory()
@@ -98,13 +104,14 @@ def _worker(rank, world, port, case, placement, q):
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("case", sorted(CASES))
 @pytest.mark.parametrize("placement", [False, True])
-def test_sharded_decode_matches_oracle(case, placement):
+@pytest.mark.parametrize("fused", [True, False], ids=["k5_nvlink", "nccl"])
+def test_sharded_decode_matches_oracle(case, placement, fused):
     import torch.multiprocessing as mp
     world = min(_ngpus(), 4)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, placement, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, placement, fused, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=600) for _ in procs)
