@@ -713,7 +713,15 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
         // ---- 3. wait for every rank's record of group g
         if (threadIdx.x < x.nranks) {
             const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(threadIdx.x) * x.slot_stride + g;
+            // a peer that never publishes (it failed before this launch) must
+            // not wedge the GPU: give up after ~10 s with a trap
+            uint64_t t0 = 0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
             while (ld_acquire_sys(f) != x.epoch) {
+                __nanosleep(64);
+                uint64_t t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                if (t1 - t0 > 10000000000ull) __trap();
             }
         }
         __syncthreads();
