@@ -150,6 +150,14 @@ dattn_status dattn_kv_write(dattn_store* s, int32_t seq, int kv_head, int64_t to
 dattn_status dattn_kv_read(dattn_store* s, int32_t seq, int kv_head, int64_t tok0, int64_t n,
                            void* k, void* v);
 
+/* KV append (the decode loop's write): every sequence in
+ * seqs[0..n) grows by one token (a page is allocated when the last one is
+ * full, RManager::alloc_local controlplane.cpp:38-44) and the new rows
+ * k_new/v_new [n][num_kv_heads][padded_dim] (store dtype, `mem` memory) are
+ * written at the new position. seqs is a HOST array. */
+dattn_status dattn_kv_append(dattn_store* s, int n, const int32_t* seqs, const void* k_new,
+                             const void* v_new, int mem);
+
 /* K4: deterministic counter-hash fill of ALL heads of tokens [0, tokens(seq))
  * of `seq` with the values of logical sequence `logical_seq`, logical token
  * logical_tok0 + t (CPU twin oracle/dattn_oracle.c). */

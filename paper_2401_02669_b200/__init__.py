@@ -128,6 +128,8 @@ _FUNCS = {
                                       ctypes.c_int]),
     "dattn_kv_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "dattn_kv_append": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int]),
     "dattn_kv_fill_synthetic": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
                                                ctypes.c_uint32, ctypes.c_int64, ctypes.c_float,
                                                ctypes.c_float]),
@@ -347,6 +349,12 @@ class Store:
             k = (k.astype(np.uint32) << 16).view(np.float32)
             v = (v.astype(np.uint32) << 16).view(np.float32)
         return k.astype(np.float64), v.astype(np.float64)
+
+    def kv_append(self, seqs: Sequence[int], k_new, v_new, mem: int = MEM_DEVICE):
+        """Append one token to each sequence: k_new/v_new [n][num_kv_heads][padded_dim]."""
+        arr = (ctypes.c_int32 * max(len(seqs), 1))(*seqs)
+        check(lib.dattn_kv_append(self._h, len(seqs), ctypes.cast(arr, ctypes.c_void_p), ptr(k_new),
+                                  ptr(v_new), mem))
 
     def fill_synthetic(self, seq: int, seed: int, logical_seq: int, logical_tok0: int = 0,
                        amp_k: float = 1.0, amp_v: float = 2.0):

@@ -905,6 +905,62 @@ dattn_status dattn_kv_read(dattn_store* s, int32_t seq, int kv_head, int64_t tok
     });
 }
 
+dattn_status dattn_kv_append(dattn_store* s, int n, const int32_t* seqs, const void* k_new,
+                             const void* v_new, int mem) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        if (n <= 0) return;
+        REQUIRE_ARG(seqs && k_new && v_new, "null argument");
+        REQUIRE_ARG(mem == DATTN_MEM_DEVICE || mem == DATTN_MEM_HOST, "bad mem kind");
+        for (int i = 0; i < n; ++i) s->check_seq(seqs[i]);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < i; ++j)
+                if (seqs[i] == seqs[j]) throw Error(DATTN_ERR_CONTRACT, "duplicate sequence in append");
+        s->activate();
+        std::vector<int32_t> meta(2 * static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            const int64_t t = s->seq_tokens[seqs[i]];
+            s->grow(seqs[i], t + 1);
+            meta[i] = seqs[i];
+            meta[n + i] = static_cast<int32_t>(t);
+        }
+        const size_t rows = static_cast<size_t>(n) * s->cfg.num_kv_heads * s->dp * s->esz;
+        DevBuf tmp;
+        tmp.ensure(meta.size() * sizeof(int32_t));
+        cuda_check(cudaMemcpyAsync(tmp.p, meta.data(), meta.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                   s->stream),
+                   "cudaMemcpyAsync");
+        const void* kd = k_new;
+        const void* vd = v_new;
+        DevBuf rowsbuf;
+        if (mem == DATTN_MEM_HOST) {
+            rowsbuf.ensure(2 * rows);
+            cuda_check(cudaMemcpyAsync(rowsbuf.p, k_new, rows, cudaMemcpyHostToDevice, s->stream), "cudaMemcpyAsync");
+            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(rowsbuf.p) + rows, v_new, rows, cudaMemcpyHostToDevice,
+                                       s->stream),
+                       "cudaMemcpyAsync");
+            kd = rowsbuf.p;
+            vd = static_cast<uint8_t*>(rowsbuf.p) + rows;
+        }
+        AppendParams p{};
+        p.k_pool = s->kpool;
+        p.v_pool = s->vpool;
+        p.block_tables = s->d_bt;
+        p.bt_stride = s->cfg.max_pages_per_seq;
+        p.page_tokens = s->cfg.page_tokens;
+        p.num_kv_heads = s->cfg.num_kv_heads;
+        p.seqs = static_cast<const int32_t*>(tmp.p);
+        p.positions = static_cast<const int32_t*>(tmp.p) + n;
+        p.k_new = kd;
+        p.v_new = vd;
+        p.n = n;
+        cuda_check(launch_append(s->cfg.dtype, s->dp, p, s->stream), "launch(append)");
+        count_launch(1);
+        // the temporaries are freed on return: finish before that
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    });
+}
+
 dattn_status dattn_kv_fill_synthetic(dattn_store* s, int32_t seq, uint64_t seed,
                                      uint32_t logical_seq, int64_t logical_tok0, float amp_k,
                                      float amp_v) {

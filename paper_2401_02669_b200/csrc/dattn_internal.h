@@ -84,6 +84,21 @@ struct FillParams {
     float amp_v;
 };
 
+// KV append: one new token row per (sequence, kv head) written into its page.
+struct AppendParams {
+    void* k_pool;
+    void* v_pool;
+    const int32_t* block_tables;
+    int32_t bt_stride;
+    int32_t page_tokens;
+    int32_t num_kv_heads;
+    const int32_t* seqs;       // [n]
+    const int32_t* positions;  // [n] token index being written
+    const void* k_new;         // [n][Hkv][DP]
+    const void* v_new;
+    int32_t n;
+};
+
 struct QFillParams {
     void* q;
     int32_t rows;
@@ -120,6 +135,7 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st);
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st);
+cudaError_t launch_append(int dtype, int dp, const AppendParams& p, cudaStream_t st);
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);
 cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
 cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st);

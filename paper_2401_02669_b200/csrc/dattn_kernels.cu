@@ -814,6 +814,27 @@ __global__ void fill_kv_kernel(const FillParams p) {
 }
 
 template <typename T, int DP>
+__global__ void append_kernel(const AppendParams p) {
+    // 16-B chunks: (sequence, kv head, chunk)
+    constexpr int kC = DP * static_cast<int>(sizeof(T)) / 16;
+    const int64_t total = static_cast<int64_t>(p.n) * p.num_kv_heads * kC;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % kC);
+        const int64_t sh = i / kC;
+        const int h = static_cast<int>(sh % p.num_kv_heads);
+        const int s = static_cast<int>(sh / p.num_kv_heads);
+        const int t = p.positions[s];
+        const int64_t page = p.block_tables[static_cast<int64_t>(p.seqs[s]) * p.bt_stride + t / p.page_tokens];
+        const int64_t dst = ((page * p.num_kv_heads + h) * p.page_tokens + t % p.page_tokens) * DP;
+        reinterpret_cast<uint4*>(static_cast<T*>(p.k_pool) + dst)[c] =
+            reinterpret_cast<const uint4*>(static_cast<const T*>(p.k_new) + sh * DP)[c];
+        reinterpret_cast<uint4*>(static_cast<T*>(p.v_pool) + dst)[c] =
+            reinterpret_cast<const uint4*>(static_cast<const T*>(p.v_new) + sh * DP)[c];
+    }
+}
+
+template <typename T, int DP>
 __global__ void fill_q_kernel(const QFillParams p) {
     const uint64_t kq = stream_key(p.seed, 3);
     const int64_t total = static_cast<int64_t>(p.rows) * p.heads * DP;
@@ -984,6 +1005,12 @@ cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid,
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st) {
     const int grid = grid_for(p.tokens * p.num_kv_heads * dp);
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (fill_kv_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append(int dtype, int dp, const AppendParams& p, cudaStream_t st) {
+    const int grid = grid_for(static_cast<int64_t>(p.n) * p.num_kv_heads * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (append_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
     return cudaGetLastError();
 }
 

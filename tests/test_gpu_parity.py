@@ -289,6 +289,43 @@ def test_kv_head_specific_ranges_and_empty_rows(torch_cuda):
     assert not out[1:].any()
 
 
+def test_kv_append_decode_loop(torch_cuda):
+    """Decode loop: append one token per step (pages allocated at page
+    boundaries, RManager::alloc_local) and attend over the grown context."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    lens0 = [14, 31, 100]
+    hq, hkv, d, seed = 8, 4, 128, 55
+    st = pb.Store(d, hq, hkv, pb.BF16, 16, 64, max_seqs=4, max_pages_per_seq=16)
+    st.set_stream(torch.cuda.current_stream().cuda_stream)
+    seqs = [st.seq_create(L) for L in lens0]
+    for b, s in enumerate(seqs):
+        st.fill_synthetic(s, seed, b, 0, 1.0, 2.0)
+    q = torch.empty(3, hq, 128, dtype=torch.bfloat16, device="cuda")
+    st.q_fill_synthetic(q, 3, seed)
+    for step in range(5):
+        kn = torch.empty(3, hkv, 128, dtype=torch.bfloat16)
+        vn = torch.empty_like(kn)
+        for b in range(3):
+            for h in range(hkv):
+                k1, v1 = oracle.synth_kv(seed, b, h, lens0[b] + step, 1, d, 1.0, 2.0, pb.BF16)
+                kn[b, h] = torch.from_numpy(k1[0])
+                vn[b, h] = torch.from_numpy(v1[0])
+        st.kv_append(seqs, kn.cuda(), vn.cuda())
+        lens = [L + step + 1 for L in lens0]
+        assert [st.seq_tokens(s) for s in seqs] == lens
+        assert [len(st.block_table(s)) for s in seqs] == [pb.blocks_for_tokens(L, 16) for L in lens]
+        out = out_np(torch, decode(torch, st, [pb.Range(s, b, 0, L) for b, (s, L) in enumerate(zip(seqs, lens))],
+                                   3, q), d)
+        ref = oracle.decode_ranges(seed, [0] * 3, lens, [0, 1, 2], hq, hkv, d, dtype=pb.BF16)
+        assert rel_errs(out, ref) < 2e-2
+    # host-memory rows give the same result
+    k, v = st.kv_read(seqs[0], 2, lens0[0], 5)
+    rk, rv = oracle.synth_kv(seed, 0, 2, lens0[0], 5, d, 1.0, 2.0, pb.BF16)
+    assert np.array_equal(k, rk) and np.array_equal(v, rv)
+
+
 def test_host_memory_e2e_matches_device(torch_cuda):
     import paper_2401_02669_b200 as pb
     torch = torch_cuda
