@@ -237,8 +237,12 @@ def run_b200_arm(args, rank, ws, local):
     w = workloads.config(args.config)
     torch.cuda.set_device(local)
     page = w.page_tokens
-    shares = plan_rank_ranges(w.lens, ws, page)[rank]
-    pages = sum(-(-rr.tokens // page) for rr in shares) + 16
+    if w.placement == "planner":
+        from paper_2401_02669_b200.sharding import placement_from_moves, planner_placement
+        homes, lent = planner_placement(w.lens, ws, page)
+        shares = placement_from_moves(w.lens, homes, lent, ws, page)[rank]
+    else:
+        pages = sum(-(-rr.tokens // page) for rr in shares) + 16
     max_pps = max(-(-rr.tokens // page) for rr in shares) + 2
     st = pb.Store(w.d, w.hq, w.hkv, w.dtype, page, pages, max_seqs=w.batch + 4,
                   max_pages_per_seq=max(max_pps, 1), device=local)
@@ -365,6 +369,7 @@ def run_b200_arm(args, rank, ws, local):
                    else "KV near L2 size: steps re-read it (L2-warm)",
                    "chunk_tokens": s.last_chunk_tokens, "ma_items": s.last_items, "ma_grid": s.ma_grid, **w.meta},
         "kv_gbs": w.kv_bytes() / (ms_step * 1e-3) / 1e9,
+        "rank0_kv_bytes": kv_rank,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel_name, "kernel_ms": ma_ms, "merge_ms": merge_ms, "allgather_ms": comm_ms,

@@ -100,7 +100,7 @@ void dattn_store::setup_exchange() {
     if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
     slot_stride = static_cast<int64_t>(cfg.max_seqs) * cfg.num_q_heads;
     const size_t xbytes = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
-    const size_t fbytes = static_cast<size_t>(nranks) * slot_stride * sizeof(uint32_t);
+    const size_t fbytes = static_cast<size_t>(nranks) * kMaxExchangeGrid * sizeof(uint32_t);
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
     cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
@@ -616,10 +616,14 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.rank = rank;
         xp.nranks = nranks;
         xp.slot_stride = slot_stride;
+        xp.flag_stride = kMaxExchangeGrid;
         xp.epoch = ++epoch;
         xp.out_norm = out_dev0;
+        // one warp per group, 8 per CTA; same grid on every rank (identical
+        // row counts), all CTAs co-resident (<= 4 per SM)
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>(static_cast<int64_t>(row_recs), static_cast<int64_t>(num_sms) * 4)));
+            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8,
+                                 std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));
         cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
         if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
         cuda_check(launch_merge_exchange(cfg.dtype, dp, xp, grid, stream), "launch(K5 merge_exchange)");

@@ -58,6 +58,7 @@ struct MergeParams {
 
 // K5: fused local merge + NVLink exchange + rank merge (one launch per step).
 constexpr int kMaxRanks = 8;
+constexpr int kMaxExchangeGrid = 1024;  // K5 CTAs (flags per source rank)
 struct XParams {
     MergeParams local;                 // chunk records of this rank (out_* unused)
     void* peer_x[kMaxRanks];           // exchange buffers of every rank (own at [rank])
@@ -65,6 +66,7 @@ struct XParams {
     int32_t rank;
     int32_t nranks;
     int64_t slot_stride;               // records per source rank in an exchange buffer
+    int64_t flag_stride;               // flags per source rank (>= grid)
     uint32_t epoch;                    // this step's flag value
     void* out_norm;                    // [rows*heads][DP] storage dtype
 };

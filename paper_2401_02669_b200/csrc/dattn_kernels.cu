@@ -609,23 +609,33 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
+// One warp per (row, q head) group; a CTA owns the groups
+// [blockIdx.x*8, blockIdx.x*8+8) + k*gridDim.x*8. Phase A: every warp merges
+// its groups' chunk records and stores the result into every rank's exchange
+// buffer (NVLink stores for peers). Phase B: one system-scope fence per CTA,
+// then one release flag per (destination rank, CTA). Phase C: wait for the
+// same CTA index of every rank. Phase D: every warp merges the nranks records
+// of its groups into the output. All ranks launch the same grid and group
+// order, and the grid is co-resident, so the waits cannot deadlock.
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const XParams x) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
     constexpr int REC = DP + 4;
-    __shared__ Acc s_max[kMergeWarps];
-    __shared__ Acc s_e[kMergeWarps];
-    __shared__ Acc s_tok[kMergeWarps];
-    __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
-    __shared__ __align__(16) Acc s_rec[REC];
+    constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
+                                           : (DP % 64 == 0 ? 2 : 1);
+    constexpr int kPer = 32 * kVW;
+    constexpr int kSweeps = (DP + kPer - 1) / kPer;
     const MergeParams& p = x.local;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
+    const int64_t gstride = static_cast<int64_t>(gridDim.x) * kMergeWarps;
+    const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp;
     const Acc* R = static_cast<const Acc*>(p.recs);
-    for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
-        // ---- 1. merge this rank's chunks of group g (K3 algorithm)
+
+    // ---- A. local merge + push to every rank
+    for (int64_t g = g0; g < groups; g += gstride) {
         const int row = static_cast<int>(g / p.heads);
         const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
         const int cbase = p.row_begin[row];
@@ -640,7 +650,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             return r[2] != Acc(0);
         };
         Acc mg = kNegInf;
-        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        for (int c = lane; c < n; c += 32) {
             const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
             if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
         }
@@ -649,116 +659,105 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
             mg = o > mg ? o : mg;
         }
-        if (lane == 0) s_max[warp] = mg;
-        __syncthreads();
-        mg = s_max[0];
-#pragma unroll
-        for (int w = 1; w < kMergeWarps; ++w) mg = s_max[w] > mg ? s_max[w] : mg;
         Acc eg = 0, ntok = 0;
-        Acc acc[(DP + 31) / 32];
+        Acc acc[kSweeps][kVW];
 #pragma unroll
-        for (int k = 0; k < (DP + 31) / 32; ++k) acc[k] = 0;
-        for (int c = warp; c < n; c += kMergeWarps) {
+        for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+        for (int c = 0; c < n; ++c) {
             const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
             if (!live(c, r)) continue;
             const Acc w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
             eg += r[1] * w;
             ntok += r[2];
 #pragma unroll
-            for (int k = 0; k < (DP + 31) / 32; ++k) {
-                const int j = lane + 32 * k;
-                if (j < DP) acc[k] += r[4 + j] * w;
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) acc[sw][v] += r[4 + j + v] * w;
             }
         }
-#pragma unroll
-        for (int k = 0; k < (DP + 31) / 32; ++k) {
-            const int j = lane + 32 * k;
-            if (j < DP) s_acc[warp][j] = acc[k];
-        }
-        if (lane == 0) {
-            s_e[warp] = eg;
-            s_tok[warp] = ntok;
-        }
-        __syncthreads();
-        for (int j = threadIdx.x; j < DP; j += blockDim.x) {
-            Acc a = 0;
-#pragma unroll
-            for (int w = 0; w < kMergeWarps; ++w) a += s_acc[w][j];
-            s_rec[4 + j] = a;
-        }
-        if (threadIdx.x == 0) {
-            Acc e_tot = 0, tok_tot = 0;
-#pragma unroll
-            for (int w = 0; w < kMergeWarps; ++w) {
-                e_tot += s_e[w];
-                tok_tot += s_tok[w];
-            }
-            s_rec[0] = tok_tot != Acc(0) ? mg : kNegInf;
-            s_rec[1] = e_tot;
-            s_rec[2] = tok_tot;
-            s_rec[3] = 0;
-        }
-        __syncthreads();
-        // ---- 2. push the record to every rank, then publish it
-        const int64_t slot = static_cast<int64_t>(x.rank) * x.slot_stride + g;
+        const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
         for (int r = 0; r < x.nranks; ++r) {
-            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot * REC;
-            for (int j = threadIdx.x; j < REC; j += blockDim.x) dst[j] = s_rec[j];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            for (int r = 0; r < x.nranks; ++r) st_release_sys(x.peer_flags[r] + slot, x.epoch);
-        }
-        // ---- 3. wait for every rank's record of group g
-        if (threadIdx.x < x.nranks) {
-            const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(threadIdx.x) * x.slot_stride + g;
-            // a peer that never publishes (it failed before this launch) must
-            // not wedge the GPU: give up after ~10 s with a trap
-            uint64_t t0 = 0;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            while (ld_acquire_sys(f) != x.epoch) {
-                __nanosleep(64);
-                uint64_t t1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-                if (t1 - t0 > 10000000000ull) __trap();
-            }
-        }
-        __syncthreads();
-        // ---- 4. rank merge (records read past L1: they were written remotely)
-        const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
-        if (warp == 0) {
-            Acc m2 = kNegInf, e2 = 0;
-            Acc a2[(DP + 31) / 32];
+            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
 #pragma unroll
-            for (int k = 0; k < (DP + 31) / 32; ++k) a2[k] = 0;
-            for (int r = 0; r < x.nranks; ++r) {
-                const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-                if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
-            }
-            Acc tok2 = 0;
-            for (int r = 0; r < x.nranks; ++r) {
-                const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-                const Acc tk = __ldcv(rec + 2);
-                if (tk == Acc(0)) continue;
-                const Acc mr = __ldcv(rec);
-                const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
-                e2 += __ldcv(rec + 1) * w;
-                tok2 += tk;
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
 #pragma unroll
-                for (int k = 0; k < (DP + 31) / 32; ++k) {
-                    const int j = lane + 32 * k;
-                    if (j < DP) a2[k] += __ldcv(rec + 4 + j) * w;
-                }
+                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
             }
-            T* o = static_cast<T*>(x.out_norm) + g * DP;
-#pragma unroll
-            for (int k = 0; k < (DP + 31) / 32; ++k) {
-                const int j = lane + 32 * k;
-                if (j < DP) o[j] = E::from_acc(tok2 != Acc(0) ? a2[k] / e2 : Acc(0));
+            if (lane == 0) {
+                dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                dst[1] = eg;
+                dst[2] = ntok;
+                dst[3] = 0;
             }
         }
-        __syncthreads();
+    }
+    // ---- B. publish: one fence for the CTA, one flag per destination rank
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int r = 0; r < x.nranks; ++r)
+            st_release_sys(x.peer_flags[r] + static_cast<int64_t>(x.rank) * x.flag_stride + blockIdx.x, x.epoch);
+    }
+    // ---- C. wait for this CTA index on every rank (bounded: a peer that
+    //      never publishes must not wedge the GPU)
+    if (threadIdx.x < x.nranks) {
+        const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(threadIdx.x) * x.flag_stride + blockIdx.x;
+        uint64_t t0 = 0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire_sys(f) != x.epoch) {
+            __nanosleep(32);
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 10000000000ull) __trap();
+        }
+    }
+    __syncthreads();
+    // ---- D. rank merge (exchange data read past L1: it was written remotely)
+    const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
+    for (int64_t g = g0; g < groups; g += gstride) {
+        Acc m2 = kNegInf;
+        for (int r = lane; r < x.nranks; r += 32) {
+            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, off));
+        Acc e2 = 0, tok2 = 0;
+        Acc a2[kSweeps][kVW];
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) a2[sw][v] = 0;
+        for (int r = 0; r < x.nranks; ++r) {
+            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            const Acc tk = __ldcv(rec + 2);
+            if (tk == Acc(0)) continue;
+            const Acc mr = __ldcv(rec);
+            const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
+            e2 += __ldcv(rec + 1) * w;
+            tok2 += tk;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) a2[sw][v] += __ldcv(rec + 4 + j + v) * w;
+            }
+        }
+        T* o = static_cast<T*>(x.out_norm) + g * DP;
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw) {
+            const int j = sw * kPer + lane * kVW;
+            if (j < DP)
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(tok2 != Acc(0) ? a2[sw][v] / e2 : Acc(0));
+        }
     }
 }
 

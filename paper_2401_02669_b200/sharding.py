@@ -97,3 +97,43 @@ def coverage_ok(per_rank: List[List[RankRange]], lens: Sequence[int]) -> bool:
         if cur != L:
             return False
     return True
+
+
+def planner_placement(lens: Sequence[int], nranks: int, block_tokens: int,
+                      retain_local_fraction: float = 0.5):
+    """Config-5 placement, the reference policy restated on block counts.
+
+    1. Dispatch: requests in order, each homed on the instance with the most
+       free blocks, i.e. the least loaded (simengine.cpp:252-257); ties go to
+       the lowest id.
+    2. Lending (gManager plan_round, scheduler.cpp:215-295): an instance above
+       the fair share ceil(total/N) lends blocks of its requests to instances
+       below it, in ascending instance id, but every request keeps at least
+       ceil(retain_local_fraction * blocks) at home (movable_blocks,
+       scheduler.cpp:425-431; retain_local_fraction scheduler.hpp:56).
+    Returns (homes, lent_blocks) for placement_from_moves.
+    """
+    nb = [_blocks(L, block_tokens) for L in lens]
+    load = [0] * nranks
+    homes = []
+    for b in nb:
+        h = min(range(nranks), key=lambda r: (load[r], r))
+        homes.append(h)
+        load[h] += b
+    target = -(-sum(nb) // nranks)
+    lent: Dict[Tuple[int, int], int] = {}
+    for req, b in enumerate(nb):
+        h = homes[req]
+        keep_min = -(-int(retain_local_fraction * b * 1000) // 1000)
+        movable = max(0, min(b - keep_min, load[h] - target))
+        for r in range(nranks):
+            if movable <= 0:
+                break
+            if r == h or load[r] >= target:
+                continue
+            take = min(movable, target - load[r])
+            lent[(req, r)] = lent.get((req, r), 0) + take
+            load[r] += take
+            load[h] -= take
+            movable -= take
+    return homes, lent

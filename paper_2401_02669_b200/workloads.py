@@ -44,6 +44,7 @@ class Workload:
     amp_k: float = 1.0
     amp_v: float = 2.0
     note: str = ""
+    placement: str = "equal"  # "equal": plan_rank_ranges; "planner": planner_placement
     meta: dict = field(default_factory=dict)
 
     @property
@@ -83,6 +84,8 @@ def config(name: str) -> Workload:
     if name in ("4", "cfg4"):
         return Workload("cfg4: 1 req x 1M tokens, LLaMA-7B MHA 32x128, bf16", [1048576], 32, 32, 128, 0)
     if name in ("5", "cfg5"):
-        return Workload("cfg5: skewed mix 1x512K + 256x2K, LLaMA-7B MHA 32x128, bf16",
-                        [524288] + [2048] * 256, 32, 32, 128, 0)
+        return Workload("cfg5: skewed mix 1x512K + 256x2K, LLaMA-7B MHA 32x128, bf16, gManager-policy placement",
+                        [524288] + [2048] * 256, 32, 32, 128, 0, placement="planner",
+                        meta={"placement": "sharding.planner_placement: least-loaded dispatch, lending "
+                                           "above fair share with >=50% of blocks kept home"})
     raise ValueError(f"unknown config {name!r}")
