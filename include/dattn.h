@@ -254,6 +254,18 @@ dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE
 dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const void* q,
                                   void* out, int mem);
 
+/* KV block migration between the GPUs of the communicator:
+ * the data path of the reference's MoveKvCache / DataTransfer protocol
+ * (controlplane.cpp:158-225, which moves descriptors only). The sender packs
+ * tokens [tok0, tok0+n) of every kv head of `seq` and ncclSend's them to
+ * `peer`; the receiver (same n) ncclRecv's and scatters them into its
+ * sequence `seq` at [tok0, tok0+n) (the receiver's sequence must already hold
+ * those positions, e.g. via dattn_seq_create / dattn_seq_resize). Paced
+ * transfers (<= 16 tokens/step, advance_transfers controlplane.cpp:205-225)
+ * are successive calls with small n. Synchronous. */
+dattn_status dattn_kv_send(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
+dattn_status dattn_kv_recv(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
+
 /* --------------------------------------------------------- verification */
 
 /* kvs_verify_attention (kvsched.h:56-62, capi.cpp:141-155) on the GPU path:

@@ -145,6 +145,8 @@ _FUNCS = {
     "dattn_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "dattn_decode_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Batch), ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_int]),
+    "dattn_kv_send": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
+    "dattn_kv_recv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
     "dattn_verify_attention": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                               ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int)]),
     "dattn_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
@@ -388,6 +390,13 @@ class Store:
                        chunk_tokens: int = 0, scale: float = 0.0):
         b, keep = _batch(ranges, num_rows, chunk_tokens, 0, scale)
         check(lib.dattn_decode_sharded(self._h, ctypes.byref(b), ptr(q), ptr(out), mem))
+
+    def kv_send(self, seq: int, tok0: int, n: int, peer: int):
+        """Migrate tokens [tok0, tok0+n) of every kv head of `seq` to `peer`."""
+        check(lib.dattn_kv_send(self._h, seq, tok0, n, peer))
+
+    def kv_recv(self, seq: int, tok0: int, n: int, peer: int):
+        check(lib.dattn_kv_recv(self._h, seq, tok0, n, peer))
 
 
 def comm_unique_id() -> bytes:

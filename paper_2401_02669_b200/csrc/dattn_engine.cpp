@@ -1081,6 +1081,54 @@ dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const vo
     });
 }
 
+static void kv_transfer(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer, bool send) {
+    if (!s->comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
+    s->check_seq(seq);
+    if (peer < 0 || peer >= s->nranks || peer == s->rank) throw Error(DATTN_ERR_CONTRACT, "bad peer rank");
+    if (tok0 < 0 || n < 0 || tok0 + n > s->seq_tokens[seq])
+        throw Error(DATTN_ERR_CONTRACT, "rows outside the sequence");
+    if (n == 0) return;
+    s->activate();
+    const size_t bytes = static_cast<size_t>(n) * s->cfg.num_kv_heads * s->dp * s->esz;
+    DevBuf buf;
+    buf.ensure(2 * bytes);
+    ScatterParams p{};
+    p.k_pool = s->kpool;
+    p.v_pool = s->vpool;
+    p.k_rows = buf.p;
+    p.v_rows = static_cast<uint8_t*>(buf.p) + bytes;
+    p.block_row = s->d_bt + static_cast<size_t>(seq) * s->cfg.max_pages_per_seq;
+    p.page_tokens = s->cfg.page_tokens;
+    p.num_kv_heads = s->cfg.num_kv_heads;
+    p.kv_head = -1;
+    p.tok0 = tok0;
+    p.n = n;
+    if (send) {
+        cuda_check(launch_gather(s->cfg.dtype, s->dp, p, s->stream), "launch(gather)");
+        count_launch(1);
+        nccl_check(ncclSend(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->stream), "ncclSend(kv)");
+    } else {
+        nccl_check(ncclRecv(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->stream), "ncclRecv(kv)");
+        cuda_check(launch_scatter(s->cfg.dtype, s->dp, p, s->stream), "launch(scatter)");
+        count_launch(1);
+    }
+    cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+}
+
+dattn_status dattn_kv_send(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        kv_transfer(s, seq, tok0, n, peer, true);
+    });
+}
+
+dattn_status dattn_kv_recv(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        kv_transfer(s, seq, tok0, n, peer, false);
+    });
+}
+
 dattn_status dattn_host_alloc(size_t bytes, void** out) {
     return guarded([&] {
         REQUIRE_ARG(out, "null argument");

@@ -851,7 +851,9 @@ __global__ void fill_q_kernel(const QFillParams p) {
 
 template <typename T, int DP>
 __global__ void scatter_kernel(const ScatterParams p) {
-    const int64_t total = p.n * DP;
+    // rows [n][DP] of one kv head, or [n][Hkv][DP] of all heads (kv_head < 0)
+    const int nh = p.kv_head < 0 ? p.num_kv_heads : 1;
+    const int64_t total = p.n * nh * DP;
     const T* ks = static_cast<const T*>(p.k_rows);
     const T* vs = static_cast<const T*>(p.v_rows);
     T* kp = static_cast<T*>(p.k_pool);
@@ -859,10 +861,12 @@ __global__ void scatter_kernel(const ScatterParams p) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int j = static_cast<int>(i % DP);
-        const int64_t t = p.tok0 + i / DP;
+        const int64_t th = i / DP;
+        const int hh = p.kv_head < 0 ? static_cast<int>(th % nh) : p.kv_head;
+        const int64_t t = p.tok0 + th / nh;
         const int64_t page = p.block_row[t / p.page_tokens];
         const int64_t dst =
-            ((page * p.num_kv_heads + p.kv_head) * p.page_tokens + t % p.page_tokens) * DP + j;
+            ((page * p.num_kv_heads + hh) * p.page_tokens + t % p.page_tokens) * DP + j;
         kp[dst] = ks[i];
         vp[dst] = vs[i];
     }
@@ -870,7 +874,8 @@ __global__ void scatter_kernel(const ScatterParams p) {
 
 template <typename T, int DP>
 __global__ void gather_kernel(const ScatterParams p) {
-    const int64_t total = p.n * DP;
+    const int nh = p.kv_head < 0 ? p.num_kv_heads : 1;
+    const int64_t total = p.n * nh * DP;
     T* ks = static_cast<T*>(const_cast<void*>(p.k_rows));
     T* vs = static_cast<T*>(const_cast<void*>(p.v_rows));
     const T* kp = static_cast<const T*>(p.k_pool);
@@ -878,10 +883,12 @@ __global__ void gather_kernel(const ScatterParams p) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int j = static_cast<int>(i % DP);
-        const int64_t t = p.tok0 + i / DP;
+        const int64_t th = i / DP;
+        const int hh = p.kv_head < 0 ? static_cast<int>(th % nh) : p.kv_head;
+        const int64_t t = p.tok0 + th / nh;
         const int64_t page = p.block_row[t / p.page_tokens];
         const int64_t src =
-            ((page * p.num_kv_heads + p.kv_head) * p.page_tokens + t % p.page_tokens) * DP + j;
+            ((page * p.num_kv_heads + hh) * p.page_tokens + t % p.page_tokens) * DP + j;
         ks[i] = kp[src];
         vs[i] = vp[src];
     }
@@ -1020,13 +1027,13 @@ cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t 
 }
 
 cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st) {
-    const int grid = grid_for(p.n * dp);
+    const int grid = grid_for(p.n * dp * (p.kv_head < 0 ? p.num_kv_heads : 1));
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (scatter_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
     return cudaGetLastError();
 }
 
 cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st) {
-    const int grid = grid_for(p.n * dp);
+    const int grid = grid_for(p.n * dp * (p.kv_head < 0 ? p.num_kv_heads : 1));
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (gather_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
     return cudaGetLastError();
 }

@@ -122,3 +122,83 @@ def test_sharded_decode_matches_oracle(case, placement, fused):
         assert agree and same
         if rank == 0:
             assert err < CASES[case]["tol"], err
+
+
+def _migrate_worker(rank, world, port, q):
+    """Rank 0 lends the tail of a request to rank 1 (MoveKvCache data path,
+    paced at 16 tokens per transfer); rank 1's pages must equal the generator
+    bit-exactly and a sharded decode over the new placement must match the
+    oracle."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2401_02669_b200 as pb
+    try:
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        seed, L, hq, hkv, d = 808, 1000, 8, 4, 128
+        split = 512  # tokens [512, 1000) move from rank 0 to rank 1
+        st = pb.Store(d, hq, hkv, pb.BF16, 16, 128, max_seqs=4, max_pages_per_seq=80, device=rank)
+        st.set_stream(torch.cuda.current_stream().cuda_stream)
+        uid = [pb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.comm_init(uid[0], rank, world)
+        ok = True
+        if rank == 0:
+            s = st.seq_create(L)
+            st.fill_synthetic(s, seed, 0, 0, 1.0, 2.0)
+            for t in range(split, L, 16):
+                st.kv_send(s, t, min(16, L - t), 1)
+            ranges = [pb.Range(s, 0, 0, split)]
+        elif rank == 1:
+            s = st.seq_create(L - split)  # hosted blocks: positions [split, L) at 0..
+            # receive into a scratch sequence laid out like the sender, then place
+            tmp = st.seq_create(L)
+            for t in range(split, L, 16):
+                st.kv_recv(tmp, t, min(16, L - t), 0)
+            for h in range(hkv):
+                k, v = st.kv_read(tmp, h, split, L - split)
+                rk, rv = oracle.synth_kv(seed, 0, h, split, L - split, d, 1.0, 2.0, pb.BF16)
+                ok &= bool(np.array_equal(k, rk) and np.array_equal(v, rv))
+            ranges = [pb.Range(tmp, 0, split, L)]
+        else:
+            ranges = []
+        qd = torch.empty(1, hq, 128, dtype=torch.bfloat16, device=f"cuda:{rank}")
+        st.q_fill_synthetic(qd, 1, seed)
+        out = torch.zeros_like(qd)
+        st.decode_sharded(ranges, 1, qd, out)
+        torch.cuda.synchronize()
+        err = None
+        if rank == 0:
+            ref = oracle.decode_ranges(seed, [0], [L], [0], hq, hkv, d, dtype=pb.BF16)
+            got = out[..., :d].double().cpu().numpy()
+            err = max(oracle.rel_err(got[0, h], ref[0, h]) for h in range(hq))
+        q.put((rank, err, ok, None))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, None, False, repr(e)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_kv_block_migration_between_gpus():
+    import torch.multiprocessing as mp
+    world = min(_ngpus(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for rank, err, ok, exc in res:
+        assert exc is None, (rank, exc)
+        assert ok
+        if rank == 0:
+            assert err < 2e-2, err
