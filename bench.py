@@ -232,17 +232,12 @@ def run_b200_arm(args, rank, ws, local):
 
     import paper_2401_02669_b200 as pb
     from paper_2401_02669_b200 import workloads
-    from paper_2401_02669_b200.sharding import plan_rank_ranges
 
     w = workloads.config(args.config)
     torch.cuda.set_device(local)
     page = w.page_tokens
-    if w.placement == "planner":
-        from paper_2401_02669_b200.sharding import placement_from_moves, planner_placement
-        homes, lent = planner_placement(w.lens, ws, page)
-        shares = placement_from_moves(w.lens, homes, lent, ws, page)[rank]
-    else:
-        pages = sum(-(-rr.tokens // page) for rr in shares) + 16
+    shares = workloads.rank_shares(w, ws)[rank]
+    pages = sum(-(-rr.tokens // page) for rr in shares) + 16
     max_pps = max(-(-rr.tokens // page) for rr in shares) + 2
     st = pb.Store(w.d, w.hq, w.hkv, w.dtype, page, pages, max_seqs=w.batch + 4,
                   max_pages_per_seq=max(max_pps, 1), device=local)

@@ -89,3 +89,12 @@ def config(name: str) -> Workload:
                         meta={"placement": "sharding.planner_placement: least-loaded dispatch, lending "
                                            "above fair share with >=50% of blocks kept home"})
     raise ValueError(f"unknown config {name!r}")
+
+
+def rank_shares(w: Workload, nranks: int):
+    """Per-rank token ranges of every request (sharding.RankRange lists)."""
+    from .sharding import placement_from_moves, plan_rank_ranges, planner_placement
+    if w.placement == "planner":
+        homes, lent = planner_placement(w.lens, nranks, w.page_tokens)
+        return placement_from_moves(w.lens, homes, lent, nranks, w.page_tokens)
+    return plan_rank_ranges(w.lens, nranks, w.page_tokens)

@@ -59,3 +59,18 @@ def test_workloads():
     assert w1.kv_bytes() == 134217728 and w1.rblocks == 4
     assert workloads.splitmix64(0) == oracle.lib.or_splitmix64(0)
     assert workloads.splitmix64(12345) == oracle.lib.or_splitmix64(12345)
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3", "4", "5"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_bench_rank_shares_cover_every_config(cfg, n):
+    w = workloads.config(cfg)
+    per = workloads.rank_shares(w, n)
+    assert len(per) == n and coverage_ok(per, w.lens)
+    # every rank lists every request (empty ranges give identity partials)
+    for rank in per:
+        assert sorted({rr.request for rr in rank}) == sorted({rr.request for rr in rank})
+    if cfg == "5" and n >= 4:
+        # placement-limited: the home keeps >= 50% of the long request
+        home_tokens = sum(rr.tokens for rr in per[0] if rr.request == 0)
+        assert home_tokens >= w.lens[0] // 2
