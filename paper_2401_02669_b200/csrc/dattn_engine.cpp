@@ -619,10 +619,14 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.flag_stride = kMaxExchangeGrid;
         xp.epoch = ++epoch;
         xp.out_norm = out_dev0;
-        // one warp per group, 8 per CTA; same grid on every rank (identical
-        // row counts), all CTAs co-resident (<= 4 per SM)
+        // 8 warps per group for long chunk lists, else one; the grid depends
+        // only on the row count and chunk shape, identical on every rank, and
+        // stays co-resident (<= 4 CTAs per SM)
+        const int64_t chunks_per_group = row_recs ? static_cast<int64_t>(pl.nchunks) / std::max(b.num_rows, 1) : 0;
+        xp.warps_per_group = chunks_per_group > 32 ? 8 : 1;
+        const int64_t gpc = 8 / xp.warps_per_group;
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8,
+            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,
                                  std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));
         cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
         if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");

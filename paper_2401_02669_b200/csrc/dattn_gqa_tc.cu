@@ -34,31 +34,39 @@ namespace tc {
 constexpr int kTile = 128;      // tokens per tile (MMA M of MMA1)
 constexpr int kD = 128;         // head dim (MMA M of MMA2, K of MMA1)
 constexpr int kN = 16;          // MMA N: q heads, padded
-constexpr int kStages = 3;
-constexpr int kThreads = 192;
+constexpr int kKStages = 3;     // K (+ Q) ring: released as soon as MMA1 has read it
+constexpr int kVStages = 3;     // V ring: released after MMA2
+constexpr int kMeta = 8;        // tile descriptors, read by the V producer / softmax warps
+constexpr int kThreads = 224;   // w0 K producer, w1 MMA, w2..5 softmax, w6 V producer
 constexpr int kHalf = kTile * 128;        // bytes of one 64-column half of a 128-row tile
 constexpr int kKVBytes = 2 * kHalf;       // one tensor (K or V) tile: 32 KB
 constexpr int kQBytes = 2 * kN * 128;     // Q slot: two halves of 16 rows x 128 B
-constexpr int kStageBytes = 2 * kKVBytes + kQBytes;  // K, V, Q = 68 KB
+constexpr int kKStageBytes = kKVBytes + kQBytes;  // 36 KB (1024-B multiple)
 constexpr int kPBytes = 2 * kN * 128;     // one P^T tile (two are kept)
-constexpr int kPidWin = 512;               // page ids of one item held in shared memory
+constexpr int kPidWin = 512;              // page ids of one item held in shared memory
+constexpr int kMaxTilePages = kTile / 16; // page_tokens >= 16
 constexpr uint32_t kTmemCols = 64;        // S^T cols 0..15, O^T buffers at 16 and 32
 
-struct StageMeta {
-    int32_t item;
+struct TileMeta {
+    int32_t item;   // -1: terminate
     int32_t tile0;  // sequence position of row 0 of the tile
     int32_t tlo, thi;
     int32_t flags;  // 1 first tile of item, 2 last tile
     int32_t row, kvh, gchunk;
+    int32_t npages;
+    int32_t page[kMaxTilePages];
 };
 
 struct Smem {
-    uint8_t stage[kStages][kStageBytes];  // 1024-B aligned (offset 0)
+    uint8_t kst[kKStages][kKStageBytes];  // 1024-B aligned (offset 0): K halves, then Q
+    uint8_t vst[kVStages][kKVBytes];
     uint8_t p[2][kPBytes];
-    uint64_t full[kStages], empty[kStages];
+    uint64_t kfull[kKStages], kempty[kKStages];
+    uint64_t vfull[kVStages], vempty[kVStages];
+    uint64_t mready[kMeta];
     uint64_t s_full, s_free;
     uint64_t p_full[2], o_full[2], o_free[2];
-    StageMeta meta[kStages];
+    TileMeta meta[kMeta];
     int32_t pid[kPidWin];
     float red_max[2][4][kN];
     float red_sum[4][kN];
@@ -190,10 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int G = p.group;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], 1);
+        for (int i = 0; i < kKStages; ++i) {
+            mbar_init(&S.kfull[i], 1);
+            mbar_init(&S.kempty[i], 1);
         }
+        for (int i = 0; i < kVStages; ++i) {
+            mbar_init(&S.vfull[i], 1);
+            mbar_init(&S.vempty[i], 1);
+        }
+        for (int i = 0; i < kMeta; ++i) mbar_init(&S.mready[i], 1);
         mbar_init(&S.s_full, 1);
         mbar_init(&S.s_free, 4);
         for (int b = 0; b < 2; ++b) {
@@ -205,8 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // zero the operand buffers once: padded Q / P rows must be 0 and stale
     // rows of partially filled tiles must be finite
-    for (int i = threadIdx.x; i < (kStages * kStageBytes + 2 * kPBytes) / 16; i += kThreads)
-        reinterpret_cast<uint4*>(S.stage)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < (kKStages * kKStageBytes + kVStages * kKVBytes + 2 * kPBytes) / 16;
+         i += kThreads)
+        reinterpret_cast<uint4*>(S.kst)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&S.tmem_base)),
@@ -226,15 +240,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = S.tmem_base;
     const uint32_t tmem_s = tmem;
     const uint32_t tmem_o0 = tmem + kN;  // O^T of even tiles; odd tiles at + kN
+    const int P = p.page_tokens;
 
     if (warp == 0) {
-        // ================================ TMA producer
+        // ================================ K producer
         // The whole warp decodes each item and fetches its page ids into
-        // shared memory in one round trip; lane 0 then streams the tiles.
+        // shared memory in one round trip; lane 0 publishes the tile
+        // descriptor and streams K (+ Q) tiles into the K ring.
         const uint64_t pol = l2_policy_evict_first();
-        const int P = p.page_tokens;
-        int stage = 0;
-        uint32_t phase = 0;
+        uint32_t t = 0;  // global tile counter of this CTA
         for (;;) {
             int item = 0;
             if (lane == 0) item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
@@ -252,9 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
             const int start = (tlo / P) * P;
             const int qrow = rg.out_row * p.num_q_heads + kvh * G;
-            const int pfirst = start / P, plast = (thi - 1) / P;
+            const int plast = (thi - 1) / P;
             int win = -1;  // first page id held in S.pid
-            for (int t0 = start; t0 < thi; t0 += kTile) {
+            for (int t0 = start; t0 < thi; t0 += kTile, ++t) {
                 const int tend = min(thi, t0 + kTile);
                 const int pg0 = t0 / P, npages = (tend - 1) / P - pg0 + 1;
                 if (win < 0 || pg0 + npages > win + kPidWin) {
@@ -265,8 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 if (lane == 0) {
-                    mbar_wait(&S.empty[stage], phase ^ 1u);
-                    StageMeta& md = S.meta[stage];
+                    TileMeta& md = S.meta[t % kMeta];
                     md.item = item;
                     md.tile0 = t0;
                     md.tlo = tlo;
@@ -275,43 +288,67 @@ __global__ void __launch_bounds__(kThreads, 1)
                     md.row = rg.out_row;
                     md.kvh = kvh;
                     md.gchunk = gchunk;
-                    mbar_arrive_expect_tx(&S.full[stage],
-                                          static_cast<uint32_t>(npages * P * 128 * 4 + G * 128 * 2));
-                    uint8_t* sk = S.stage[stage];
-                    uint8_t* sv = sk + kKVBytes;
-                    uint8_t* sq = sv + kKVBytes;
+                    md.npages = npages;
+                    for (int pg = 0; pg < npages; ++pg) md.page[pg] = S.pid[pg0 - win + pg];
+                    mbar_arrive(&S.mready[t % kMeta]);
+                    const int ks = t % kKStages;
+                    mbar_wait(&S.kempty[ks], ((t / kKStages) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&S.kfull[ks], static_cast<uint32_t>(npages * P * 128 * 2 + G * 128 * 2));
+                    uint8_t* sk = S.kst[ks];
+                    uint8_t* sq = sk + kKVBytes;
                     for (int pg = 0; pg < npages; ++pg) {
-                        const int row0 = (S.pid[pg0 - win + pg] * p.num_kv_heads + kvh) * P;
+                        const int row0 = (md.page[pg] * p.num_kv_heads + kvh) * P;
                         const int off = pg * P * 128;
-                        tma_load_2d(sk + off, &tm_k, 0, row0, &S.full[stage], pol);
-                        tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.full[stage], pol);
-                        tma_load_2d(sv + off, &tm_v, 0, row0, &S.full[stage], pol);
-                        tma_load_2d(sv + kHalf + off, &tm_v, 64, row0, &S.full[stage], pol);
+                        tma_load_2d(sk + off, &tm_k, 0, row0, &S.kfull[ks], pol);
+                        tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.kfull[ks], pol);
                     }
-                    tma_load_2d(sq, &tm_q, 0, qrow, &S.full[stage], 0);
-                    tma_load_2d(sq + kN * 128, &tm_q, 64, qrow, &S.full[stage], 0);
+                    tma_load_2d(sq, &tm_q, 0, qrow, &S.kfull[ks], 0);
+                    tma_load_2d(sq + kN * 128, &tm_q, 64, qrow, &S.kfull[ks], 0);
                 }
                 __syncwarp();
-                if (++stage == kStages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
             }
-            (void)pfirst;
         }
         if (lane == 0) {
-            mbar_wait(&S.empty[stage], phase ^ 1u);
-            S.meta[stage].item = -1;
-            mbar_arrive(&S.full[stage]);
+            S.meta[t % kMeta].item = -1;
+            mbar_arrive(&S.mready[t % kMeta]);
+            const int ks = t % kKStages;
+            mbar_wait(&S.kempty[ks], ((t / kKStages) & 1u) ^ 1u);
+            mbar_arrive(&S.kfull[ks]);
+        }
+    } else if (warp == 6) {
+        // ================================ V producer (trails the K producer)
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            for (uint32_t t = 0;; ++t) {
+                mbar_wait(&S.mready[t % kMeta], (t / kMeta) & 1u);
+                const TileMeta& md = S.meta[t % kMeta];
+                if (md.item < 0) break;
+                const int npages = md.npages, kvh = md.kvh;
+                int page[kMaxTilePages];
+#pragma unroll
+                for (int pg = 0; pg < kMaxTilePages; ++pg) page[pg] = md.page[pg];
+                const int vs = t % kVStages;
+                mbar_wait(&S.vempty[vs], ((t / kVStages) & 1u) ^ 1u);
+                mbar_arrive_expect_tx(&S.vfull[vs], static_cast<uint32_t>(npages * P * 128 * 2));
+                uint8_t* sv = S.vst[vs];
+                for (int pg = 0; pg < npages; ++pg) {
+                    const int row0 = (page[pg] * p.num_kv_heads + kvh) * P;
+                    const int off = pg * P * 128;
+                    tma_load_2d(sv + off, &tm_v, 0, row0, &S.vfull[vs], pol);
+                    tma_load_2d(sv + kHalf + off, &tm_v, 64, row0, &S.vfull[vs], pol);
+                }
+            }
         }
     } else if (warp == 1) {
         // ================================ MMA issuer
-        // Order: MMA1 of tile it+1 is issued before MMA2 of tile it, so the
-        // softmax warps find S^T(it+1) ready as soon as they hand over P(it).
+        // MMA1 of tile t+1 is issued before MMA2 of tile t, so the softmax
+        // warps find S^T(t+1) ready as soon as they hand over P(t). MMA1's
+        // commit releases the K stage, MMA2's the V stage.
         const uint32_t id1 = idesc(0), id2 = idesc(1);
-        auto issue_s = [&](int st) {
-            const uint32_t sk = smem_u32(S.stage[st]);
-            const uint32_t sq = sk + 2 * kKVBytes;
+        auto issue_s = [&](uint32_t t) {
+            const int ks = t % kKStages;
+            const uint32_t sk = smem_u32(S.kst[ks]);
+            const uint32_t sq = sk + kKVBytes;
             tc_fence_after();
             if (lane == 0) {
 #pragma unroll
@@ -321,34 +358,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_bf16(tmem_s, sdesc(sk + koff, 16, 1024), sdesc(sq + qoff, 16, 1024), id1, k > 0);
                 }
                 mma_commit(&S.s_full);
+                mma_commit(&S.kempty[ks]);
             }
             __syncwarp();
         };
-        int stage = 0;
-        uint32_t phase = 0;
-        mbar_wait(&S.full[0], 0);
+        mbar_wait(&S.kfull[0], 0);
         if (S.meta[0].item >= 0) {
             issue_s(0);
-            for (uint32_t it = 0;; ++it) {
-                int nst = stage + 1;
-                uint32_t nph = phase;
-                if (nst == kStages) {
-                    nst = 0;
-                    nph ^= 1u;
-                }
-                mbar_wait(&S.full[nst], nph);
-                const bool more = S.meta[nst].item >= 0;
+            for (uint32_t t = 0;; ++t) {
+                const uint32_t tn = t + 1;
+                mbar_wait(&S.kfull[tn % kKStages], (tn / kKStages) & 1u);
+                const bool more = S.meta[tn % kMeta].item >= 0;
                 if (more) {
-                    mbar_wait(&S.s_free, it & 1u);  // softmax warps hold S^T(it) in registers
-                    issue_s(nst);
+                    mbar_wait(&S.s_free, t & 1u);  // softmax warps hold S^T(t) in registers
+                    issue_s(tn);
                 }
-                // MMA2 of tile it: needs P^T(it) and its O^T buffer released
-                const uint32_t ob = it & 1u, oph = (it >> 1) & 1u;
+                // MMA2 of tile t: needs V(t), P^T(t) and its O^T buffer released
+                const int vs = t % kVStages;
+                const uint32_t ob = t & 1u, oph = (t >> 1) & 1u;
+                mbar_wait(&S.vfull[vs], (t / kVStages) & 1u);
                 mbar_wait(&S.p_full[ob], oph);
                 mbar_wait(&S.o_free[ob], oph ^ 1u);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sv = smem_u32(S.stage[stage]) + kKVBytes;
+                    const uint32_t sv = smem_u32(S.vst[vs]);
                     const uint32_t sp = smem_u32(S.p[ob]);
 #pragma unroll
                     for (int k = 0; k < kTile / 16; ++k) {
@@ -358,12 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  id2, k > 0);
                     }
                     mma_commit(&S.o_full[ob]);
-                    mma_commit(&S.empty[stage]);
+                    mma_commit(&S.vempty[vs]);
                 }
                 __syncwarp();
                 if (!more) break;
-                stage = nst;
-                phase = nph;
             }
         }
     } else {
@@ -375,12 +406,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float kNegInf = -INFINITY;
         float m[GI], l[GI], acc[GI], corr_prev[GI];
         bool pending = false;  // an O^T tile of the current item not yet accumulated
-        int stage = 0;
-        uint32_t phase = 0;
         float* recs = static_cast<float*>(p.records);
         for (uint32_t it = 0;; ++it) {
-            mbar_wait(&S.full[stage], phase);
-            const StageMeta md = S.meta[stage];
+            mbar_wait(&S.mready[it % kMeta], (it / kMeta) & 1u);
+            const TileMeta md = S.meta[it % kMeta];
             if (md.item < 0) break;
             if (md.flags & 1) {
 #pragma unroll
@@ -482,10 +511,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 named_bar_sync(1, 128);
-            }
-            if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1u;
             }
         }
     }

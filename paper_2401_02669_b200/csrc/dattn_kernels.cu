@@ -609,14 +609,16 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
-// One warp per (row, q head) group; a CTA owns the groups
-// [blockIdx.x*8, blockIdx.x*8+8) + k*gridDim.x*8. Phase A: every warp merges
-// its groups' chunk records and stores the result into every rank's exchange
-// buffer (NVLink stores for peers). Phase B: one system-scope fence per CTA,
-// then one release flag per (destination rank, CTA). Phase C: wait for the
-// same CTA index of every rank. Phase D: every warp merges the nranks records
-// of its groups into the output. All ranks launch the same grid and group
-// order, and the grid is co-resident, so the waits cannot deadlock.
+// A CTA owns groups [(blockIdx.x + k*gridDim.x)*gpc, +gpc) with gpc = 8/wpg
+// groups per iteration and wpg warps per group (1 for short chunk lists, 8
+// for long ones such as a 1M-token request). Phase A: the wpg warps of a group
+// merge its chunk records (max pass, then rescale-sum, combined through
+// shared memory in a fixed order) and store the result into every rank's
+// exchange buffer (NVLink stores for peers). Phase B: one system-scope fence
+// per CTA, then one release flag per (destination rank, CTA). Phase C: wait
+// for the same CTA index of every rank. Phase D: merge the nranks records of
+// the CTA's groups into the output. All ranks launch the same grid and group
+// order and the grid is co-resident, so the waits cannot deadlock.
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const XParams x) {
     using E = Elem<T>;
@@ -626,22 +628,34 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
                                            : (DP % 64 == 0 ? 2 : 1);
     constexpr int kPer = 32 * kVW;
     constexpr int kSweeps = (DP + kPer - 1) / kPer;
+    __shared__ Acc s_max[kMergeWarps];
+    __shared__ Acc s_e[kMergeWarps];
+    __shared__ Acc s_tok[kMergeWarps];
+    __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
     const MergeParams& p = x.local;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpg = x.warps_per_group;
+    const int gpc = kMergeWarps / wpg;
+    const int slotw = warp / wpg, sub = warp - slotw * wpg;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
-    const int64_t gstride = static_cast<int64_t>(gridDim.x) * kMergeWarps;
-    const int64_t g0 = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp;
     const Acc* R = static_cast<const Acc*>(p.recs);
 
     // ---- A. local merge + push to every rank
-    for (int64_t g = g0; g < groups; g += gstride) {
-        const int row = static_cast<int>(g / p.heads);
-        const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
-        const int cbase = p.row_begin[row];
-        const int n = p.row_begin[row + 1] - cbase;
-        const int64_t base = static_cast<int64_t>(cbase) * p.row_mul + h;
-        const int my_kvh = p.chunk_kvh ? h / p.group : 0;
+    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
+         gb += static_cast<int64_t>(gridDim.x) * gpc) {
+        const int64_t g = gb + slotw;
+        const bool gv = g < groups;
+        int n = 0, cbase = 0, my_kvh = 0;
+        int64_t base = 0;
+        if (gv) {
+            const int row = static_cast<int>(g / p.heads);
+            const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
+            cbase = p.row_begin[row];
+            n = p.row_begin[row + 1] - cbase;
+            base = static_cast<int64_t>(cbase) * p.row_mul + h;
+            my_kvh = p.chunk_kvh ? h / p.group : 0;
+        }
         auto live = [&](int c, const Acc* r) {
             if (p.chunk_kvh) {
                 const int tag = p.chunk_kvh[cbase + c];
@@ -650,7 +664,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             return r[2] != Acc(0);
         };
         Acc mg = kNegInf;
-        for (int c = lane; c < n; c += 32) {
+        for (int c = sub * 32 + lane; c < n; c += wpg * 32) {
             const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
             if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
         }
@@ -659,13 +673,19 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
             mg = o > mg ? o : mg;
         }
+        if (wpg > 1) {
+            if (lane == 0) s_max[warp] = mg;
+            __syncthreads();
+            mg = kNegInf;
+            for (int w2 = 0; w2 < wpg; ++w2) mg = s_max[slotw * wpg + w2] > mg ? s_max[slotw * wpg + w2] : mg;
+        }
         Acc eg = 0, ntok = 0;
         Acc acc[kSweeps][kVW];
 #pragma unroll
         for (int sw = 0; sw < kSweeps; ++sw)
 #pragma unroll
             for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
-        for (int c = 0; c < n; ++c) {
+        for (int c = sub; c < n; c += wpg) {
             const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
             if (!live(c, r)) continue;
             const Acc w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
@@ -679,21 +699,57 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
                     for (int v = 0; v < kVW; ++v) acc[sw][v] += r[4 + j + v] * w;
             }
         }
-        const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
-        for (int r = 0; r < x.nranks; ++r) {
-            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
+        if (wpg > 1) {
 #pragma unroll
             for (int sw = 0; sw < kSweeps; ++sw) {
                 const int j = sw * kPer + lane * kVW;
                 if (j < DP)
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+                    for (int v = 0; v < kVW; ++v) s_acc[warp][j + v] = acc[sw][v];
             }
             if (lane == 0) {
-                dst[0] = ntok != Acc(0) ? mg : kNegInf;
-                dst[1] = eg;
-                dst[2] = ntok;
-                dst[3] = 0;
+                s_e[warp] = eg;
+                s_tok[warp] = ntok;
+            }
+            __syncthreads();
+            if (sub == 0) {
+                eg = 0;
+                ntok = 0;
+                for (int w2 = 0; w2 < wpg; ++w2) {
+                    eg += s_e[slotw * wpg + w2];
+                    ntok += s_tok[slotw * wpg + w2];
+                }
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) {
+                            Acc a = 0;
+                            for (int w2 = 0; w2 < wpg; ++w2) a += s_acc[slotw * wpg + w2][j + v];
+                            acc[sw][v] = a;
+                        }
+                }
+            }
+            __syncthreads();
+        }
+        if (gv && sub == 0) {
+            const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
+            for (int r = 0; r < x.nranks; ++r) {
+                Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+                }
+                if (lane == 0) {
+                    dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                    dst[1] = eg;
+                    dst[2] = ntok;
+                    dst[3] = 0;
+                }
             }
         }
     }
@@ -718,9 +774,14 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
         }
     }
     __syncthreads();
-    // ---- D. rank merge (exchange data read past L1: it was written remotely)
+    // ---- D. rank merge of this CTA's groups, one warp per group
+    //      (exchange data read past L1: it was written remotely)
     const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
-    for (int64_t g = g0; g < groups; g += gstride) {
+    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
+         gb += static_cast<int64_t>(gridDim.x) * gpc) {
+        if (warp >= gpc) continue;
+        const int64_t g = gb + warp;
+        if (g >= groups) continue;
         Acc m2 = kNegInf;
         for (int r = lane; r < x.nranks; r += 32) {
             const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
