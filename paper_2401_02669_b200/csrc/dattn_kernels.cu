@@ -634,17 +634,21 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
     const MergeParams& p = x.local;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // groups per CTA iteration is fixed at 8 (rank-independent mapping);
+    // wpg only decides whether a warp or the whole CTA merges one group
     const int wpg = x.warps_per_group;
-    const int gpc = kMergeWarps / wpg;
-    const int slotw = warp / wpg, sub = warp - slotw * wpg;
+    constexpr int gpc = kMergeWarps;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     const Acc* R = static_cast<const Acc*>(p.recs);
 
     // ---- A. local merge + push to every rank
     for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
-         gb += static_cast<int64_t>(gridDim.x) * gpc) {
-        const int64_t g = gb + slotw;
+         gb += static_cast<int64_t>(gridDim.x) * gpc)
+    for (int rep = 0; rep < (wpg == 1 ? 1 : gpc); ++rep) {
+        const int slotw = wpg == 1 ? warp : 0;
+        const int sub = wpg == 1 ? 0 : warp;
+        const int64_t g = gb + (wpg == 1 ? warp : rep);
         const bool gv = g < groups;
         int n = 0, cbase = 0, my_kvh = 0;
         int64_t base = 0;
