@@ -622,8 +622,10 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         // 8 warps per group for long chunk lists, else one; the grid depends
         // only on the row count and chunk shape, identical on every rank, and
         // stays co-resident (<= 4 CTAs per SM)
-        const int64_t chunks_per_group = row_recs ? static_cast<int64_t>(pl.nchunks) / std::max(b.num_rows, 1) : 0;
-        xp.warps_per_group = chunks_per_group > 32 ? 8 : 1;  // local choice, may differ per rank
+        int32_t max_row_chunks = 0;
+        for (int rr = 0; rr < b.num_rows; ++rr)
+            max_row_chunks = std::max(max_row_chunks, pl.words[pl.off_rowchunk + rr + 1] - pl.words[pl.off_rowchunk + rr]);
+        xp.warps_per_group = max_row_chunks > 64 ? 8 : 1;  // local choice, may differ per rank
         const int64_t gpc = 8;                                // rank-independent CTA -> groups map
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,

@@ -470,6 +470,63 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
 // summed through shared memory in a fixed order (deterministic).
 constexpr int kMergeWarps = 8;
 
+// Rescale-sum of the live chunk records c = sub + stride*i (< n) of one group:
+// lanes first compute the weights w = exp(m - m_g) of 32 records in parallel,
+// then the warp folds the records' ma vectors (lane-owned kVW-element slices,
+// independent vector loads) with the broadcast weights. Dead records get
+// w = 0; identity records hold ma = 0, so adding them changes nothing and a
+// single live record is reproduced exactly. Returns warp-reduced (e, tokens).
+template <typename Acc, int DP, int kVW, int kSweeps, typename LiveF>
+__device__ __forceinline__ void fold_chunks(const Acc* R, int64_t base, int64_t c_stride, int n, int sub,
+                                            int stride, Acc mg, LiveF live, Acc (&acc)[kSweeps][kVW],
+                                            Acc& eg, Acc& ntok, int lane) {
+    constexpr int REC = DP + 4;
+    constexpr int kPer = 32 * kVW;
+    Acc e_l = 0, t_l = 0;
+    for (int i0 = 0; sub + stride * i0 < n; i0 += 32) {
+        const int c = sub + stride * (i0 + lane);
+        Acc w = 0;
+        if (c < n) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * c_stride) * REC;
+            if (live(c, r)) {
+                w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
+                e_l += r[1] * w;
+                t_l += r[2];
+            }
+        }
+        const int cnt = min(32, (n - sub - stride * i0 + stride - 1) / stride);
+#pragma unroll 4
+        for (int k = 0; k < cnt; ++k) {
+            const Acc wk = __shfl_sync(0xffffffffu, w, k);
+            const Acc* r = R + (base + static_cast<int64_t>(sub + stride * (i0 + k)) * c_stride) * REC;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP) {
+                    if constexpr (kVW == 4) {
+                        const float4 x = *reinterpret_cast<const float4*>(r + 4 + j);
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                        acc[sw][2] += x.z * wk; acc[sw][3] += x.w * wk;
+                    } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
+                        const double2 x = *reinterpret_cast<const double2*>(r + 4 + j);
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) acc[sw][v] += r[4 + j + v] * wk;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        e_l += __shfl_xor_sync(0xffffffffu, e_l, off);
+        t_l += __shfl_xor_sync(0xffffffffu, t_l, off);
+    }
+    eg = e_l;
+    ntok = t_l;
+}
+
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergeParams p) {
     using E = Elem<T>;
@@ -532,30 +589,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
     for (int s = 0; s < kSweeps; ++s)
 #pragma unroll
         for (int v = 0; v < kVW; ++v) acc[s][v] = 0;
-    for (int c = warp; c < n; c += kMergeWarps) {
-        const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
-        if (!live(c, r)) continue;
-        const Acc mc = r[0];
-        const Acc w = (mc == mg) ? Acc(1) : exp(mc - mg);
-        eg += r[1] * w;
-        ntok += r[2];
-#pragma unroll
-        for (int s = 0; s < kSweeps; ++s) {
-            const int j = s * kPer + lane * kVW;
-            if (j < DP) {
-                if constexpr (kVW == 4) {
-                    const float4 x = *reinterpret_cast<const float4*>(r + 4 + j);
-                    acc[s][0] += x.x * w; acc[s][1] += x.y * w; acc[s][2] += x.z * w; acc[s][3] += x.w * w;
-                } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
-                    const double2 x = *reinterpret_cast<const double2*>(r + 4 + j);
-                    acc[s][0] += x.x * w; acc[s][1] += x.y * w;
-                } else {
-#pragma unroll
-                    for (int v = 0; v < kVW; ++v) acc[s][v] += r[4 + j + v] * w;
-                }
-            }
-        }
-    }
+    fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.c_stride, n, warp, kMergeWarps, mg, live, acc, eg, ntok, lane);
 #pragma unroll
     for (int s = 0; s < kSweeps; ++s) {
         const int j = s * kPer + lane * kVW;
@@ -689,20 +723,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
         for (int sw = 0; sw < kSweeps; ++sw)
 #pragma unroll
             for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
-        for (int c = sub; c < n; c += wpg) {
-            const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
-            if (!live(c, r)) continue;
-            const Acc w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
-            eg += r[1] * w;
-            ntok += r[2];
-#pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP)
-#pragma unroll
-                    for (int v = 0; v < kVW; ++v) acc[sw][v] += r[4 + j + v] * w;
-            }
-        }
+        fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.c_stride, n, sub, wpg, mg, live, acc, eg, ntok, lane);
         if (wpg > 1) {
 #pragma unroll
             for (int sw = 0; sw < kSweeps; ++sw) {
