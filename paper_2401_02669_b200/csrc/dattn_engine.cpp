@@ -323,7 +323,7 @@ void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl)
         int64_t p2 = 1;
         while (p2 * 2 <= c) p2 *= 2;
         const int64_t lo = tc_ok ? 128 : std::max<int64_t>(ma_stage_tokens(cfg.dtype, dp), 64);
-        C = std::min<int64_t>(std::max<int64_t>(p2, lo), 2048);
+        C = std::min<int64_t>(std::max<int64_t>(p2, lo), 8192);
         if (C % cfg.page_tokens) C = (C / cfg.page_tokens + 1) * cfg.page_tokens;
     }
     if (C > INT32_MAX) throw Error(DATTN_ERR_CONTRACT, "chunk too long");
@@ -625,8 +625,12 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         int32_t max_row_chunks = 0;
         for (int rr = 0; rr < b.num_rows; ++rr)
             max_row_chunks = std::max(max_row_chunks, pl.words[pl.off_rowchunk + rr + 1] - pl.words[pl.off_rowchunk + rr]);
-        xp.warps_per_group = max_row_chunks > 64 ? 8 : 1;  // local choice, may differ per rank
-        const int64_t gpc = 8;                                // rank-independent CTA -> groups map
+        // groups per CTA iteration: 8 when groups are plentiful, else 1 so few
+        // heavy groups still spread over many CTAs -- a function of rows x heads
+        // only, hence identical on every rank. Warps per group is a local choice.
+        const int64_t gpc = static_cast<int64_t>(row_recs) >= 16LL * num_sms ? 8 : 1;
+        xp.groups_per_cta = static_cast<int32_t>(gpc);
+        xp.warps_per_group = (gpc == 1 || max_row_chunks > 64) ? 8 : 1;
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,
                                  std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));

@@ -68,7 +68,8 @@ struct XParams {
     int64_t slot_stride;               // records per source rank in an exchange buffer
     int64_t flag_stride;               // flags per source rank (>= grid)
     uint32_t epoch;                    // this step's flag value
-    int32_t warps_per_group;           // 1 or 8 (long chunk lists)
+    int32_t warps_per_group;           // 1 or 8 (long chunk lists); local choice
+    int32_t groups_per_cta;            // 8 or 1; identical on every rank
     void* out_norm;                    // [rows*heads][DP] storage dtype
 };
 

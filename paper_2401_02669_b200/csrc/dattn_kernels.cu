@@ -99,6 +99,18 @@ struct Layout {
     }
 };
 
+// Blackwell packed fp32 FMA (SASS FFMA2): (d0, d1) += (a0, a1) * (b0, b1).
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%0, %1};\n\t"
+        "fma.rn.f32x2 rc, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rc;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 __device__ __forceinline__ int find_range(const int32_t* prefix, int n, int item) {
     // largest r with prefix[r] <= item (prefix[0] == 0, prefix[n] > item)
     int lo = 0, hi = n;
@@ -293,8 +305,9 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                     valid[u] = t < n;
                     const int tc = valid[u] ? t : n - 1;
                     const uint4* rowp = reinterpret_cast<const uint4*>(ks + tc * DP);
+                    Acc s2[HPW][2];
 #pragma unroll
-                    for (int hs = 0; hs < HPW; ++hs) s[u][hs] = 0;
+                    for (int hs = 0; hs < HPW; ++hs) s2[hs][0] = s2[hs][1] = 0;
 #pragma unroll
                     for (int c = 0; c < CPL; ++c) {
                         const uint4 ch = rowp[c * LPT + sub];
@@ -305,10 +318,20 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                             for (int v = 0; v < VEC; ++v) nonfinite |= !isfinite(x[v]);
                         }
 #pragma unroll
-                        for (int hs = 0; hs < HPW; ++hs)
+                        for (int hs = 0; hs < HPW; ++hs) {
+                            if constexpr (std::is_same<Acc, float>::value) {
 #pragma unroll
-                            for (int v = 0; v < VEC; ++v) s[u][hs] += q[hs][c * VEC + v] * x[v];
+                                for (int v = 0; v < VEC; v += 2)
+                                    ffma2(s2[hs][0], s2[hs][1], q[hs][c * VEC + v], q[hs][c * VEC + v + 1], x[v],
+                                          x[v + 1]);
+                            } else {
+#pragma unroll
+                                for (int v = 0; v < VEC; ++v) s2[hs][v & 1] += q[hs][c * VEC + v] * x[v];
+                            }
+                        }
                     }
+#pragma unroll
+                    for (int hs = 0; hs < HPW; ++hs) s[u][hs] = s2[hs][0] + s2[hs][1];
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
@@ -333,8 +356,12 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                     }
                     e[hs] = es;
                     m[hs] = mx;
+                    // the running max rarely moves after the first tokens: skip
+                    // the rescale when no token group of the warp needs it
+                    if (__any_sync(0xffffffffu, corr != Acc(1))) {
 #pragma unroll
-                    for (int i = 0; i < EPL; ++i) acc[hs][i] *= corr;
+                        for (int i = 0; i < EPL; ++i) acc[hs][i] *= corr;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -351,10 +378,17 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                             for (int v = 0; v < VEC; ++v) nonfinite |= !isfinite(x[v]);
                         }
 #pragma unroll
-                        for (int hs = 0; hs < HPW; ++hs)
+                        for (int hs = 0; hs < HPW; ++hs) {
+                            if constexpr (std::is_same<Acc, float>::value) {
 #pragma unroll
-                            for (int v = 0; v < VEC; ++v)
-                                acc[hs][c * VEC + v] += pw[u][hs] * x[v];
+                                for (int v = 0; v < VEC; v += 2)
+                                    ffma2(acc[hs][c * VEC + v], acc[hs][c * VEC + v + 1], pw[u][hs], pw[u][hs],
+                                          x[v], x[v + 1]);
+                            } else {
+#pragma unroll
+                                for (int v = 0; v < VEC; ++v) acc[hs][c * VEC + v] += pw[u][hs] * x[v];
+                            }
+                        }
                     }
                 }
             }
@@ -671,7 +705,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     // groups per CTA iteration is fixed at 8 (rank-independent mapping);
     // wpg only decides whether a warp or the whole CTA merges one group
     const int wpg = x.warps_per_group;
-    constexpr int gpc = kMergeWarps;
+    const int gpc = x.groups_per_cta;  // 1 or kMergeWarps
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     const Acc* R = static_cast<const Acc*>(p.recs);
@@ -680,10 +714,12 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
          gb += static_cast<int64_t>(gridDim.x) * gpc)
     for (int rep = 0; rep < (wpg == 1 ? 1 : gpc); ++rep) {
+        // wpg == 1 (only with gpc == 8): warp w merges group gb + w;
+        // wpg == 8: the whole CTA merges group gb + rep
         const int slotw = wpg == 1 ? warp : 0;
         const int sub = wpg == 1 ? 0 : warp;
         const int64_t g = gb + (wpg == 1 ? warp : rep);
-        const bool gv = g < groups;
+        const bool gv = g < groups && (wpg == 1 ? warp < gpc : true);
         int n = 0, cbase = 0, my_kvh = 0;
         int64_t base = 0;
         if (gv) {
