@@ -702,65 +702,116 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
     const MergeParams& p = x.local;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // groups per CTA iteration is fixed at 8 (rank-independent mapping);
-    // wpg only decides whether a warp or the whole CTA merges one group
-    const int wpg = x.warps_per_group;
-    const int gpc = x.groups_per_cta;  // 1 or kMergeWarps
+    const int gpc = x.groups_per_cta;  // 1 or kMergeWarps; identical on every rank
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     const Acc* R = static_cast<const Acc*>(p.recs);
 
-    // ---- A. local merge + push to every rank
-    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
-         gb += static_cast<int64_t>(gridDim.x) * gpc)
-    for (int rep = 0; rep < (wpg == 1 ? 1 : gpc); ++rep) {
-        // wpg == 1 (only with gpc == 8): warp w merges group gb + w;
-        // wpg == 8: the whole CTA merges group gb + rep
-        const int slotw = wpg == 1 ? warp : 0;
-        const int sub = wpg == 1 ? 0 : warp;
-        const int64_t g = gb + (wpg == 1 ? warp : rep);
-        const bool gv = g < groups && (wpg == 1 ? warp < gpc : true);
-        int n = 0, cbase = 0, my_kvh = 0;
-        int64_t base = 0;
-        if (gv) {
-            const int row = static_cast<int>(g / p.heads);
-            const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
-            cbase = p.row_begin[row];
-            n = p.row_begin[row + 1] - cbase;
-            base = static_cast<int64_t>(cbase) * p.row_mul + h;
-            my_kvh = p.chunk_kvh ? h / p.group : 0;
-        }
-        auto live = [&](int c, const Acc* r) {
-            if (p.chunk_kvh) {
-                const int tag = p.chunk_kvh[cbase + c];
-                if (tag >= 0 && tag != my_kvh) return false;
-            }
-            return r[2] != Acc(0);
-        };
-        Acc mg = kNegInf;
-        for (int c = sub * 32 + lane; c < n; c += wpg * 32) {
-            const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
-            if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
-        }
+    // ---- A. local merge + push to every rank. Light groups (<= kHeavy chunk
+    //      records) are merged by one warp each, in parallel; heavy groups by
+    //      the whole CTA, one after the other.
+    constexpr int kHeavy = 64;
+    auto group_shape = [&](int64_t g, int& n, int& cbase, int64_t& base, int& my_kvh) {
+        const int row = static_cast<int>(g / p.heads);
+        const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
+        cbase = p.row_begin[row];
+        n = p.row_begin[row + 1] - cbase;
+        base = static_cast<int64_t>(cbase) * p.row_mul + h;
+        my_kvh = p.chunk_kvh ? h / p.group : 0;
+    };
+    auto push = [&](int64_t g, const Acc (&acc)[kSweeps][kVW], Acc mg, Acc eg, Acc ntok) {
+        const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
+        for (int r = 0; r < x.nranks; ++r) {
+            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
-            mg = o > mg ? o : mg;
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+            }
+            if (lane == 0) {
+                dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                dst[1] = eg;
+                dst[2] = ntok;
+                dst[3] = 0;
+            }
         }
-        if (wpg > 1) {
+    };
+    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
+         gb += static_cast<int64_t>(gridDim.x) * gpc) {
+        // light groups: warp w takes group gb + w
+        if (warp < gpc && gb + warp < groups) {
+            const int64_t g = gb + warp;
+            int n, cbase, my_kvh;
+            int64_t base;
+            group_shape(g, n, cbase, base, my_kvh);
+            if (n <= kHeavy) {
+                auto live = [&](int c, const Acc* r) {
+                    if (p.chunk_kvh) {
+                        const int tag = p.chunk_kvh[cbase + c];
+                        if (tag >= 0 && tag != my_kvh) return false;
+                    }
+                    return r[2] != Acc(0);
+                };
+                Acc mg = kNegInf;
+                for (int c = lane; c < n; c += 32) {
+                    const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+                    if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+                    mg = o > mg ? o : mg;
+                }
+                Acc eg, ntok;
+                Acc acc[kSweeps][kVW];
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+                fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.c_stride, n, 0, 1, mg, live, acc, eg, ntok, lane);
+                push(g, acc, mg, eg, ntok);
+            }
+        }
+        // heavy groups: the whole CTA, 8 warps striding over the chunk records
+        for (int rep = 0; rep < gpc; ++rep) {
+            const int64_t g = gb + rep;
+            if (g >= groups) break;
+            int n, cbase, my_kvh;
+            int64_t base;
+            group_shape(g, n, cbase, base, my_kvh);
+            if (n <= kHeavy) continue;  // uniform across the CTA
+            auto live = [&](int c, const Acc* r) {
+                if (p.chunk_kvh) {
+                    const int tag = p.chunk_kvh[cbase + c];
+                    if (tag >= 0 && tag != my_kvh) return false;
+                }
+                return r[2] != Acc(0);
+            };
+            Acc mg = kNegInf;
+            for (int c = threadIdx.x; c < n; c += blockDim.x) {
+                const Acc* r = R + (base + static_cast<int64_t>(c) * p.c_stride) * REC;
+                if (live(c, r)) mg = r[0] > mg ? r[0] : mg;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+                mg = o > mg ? o : mg;
+            }
             if (lane == 0) s_max[warp] = mg;
             __syncthreads();
-            mg = kNegInf;
-            for (int w2 = 0; w2 < wpg; ++w2) mg = s_max[slotw * wpg + w2] > mg ? s_max[slotw * wpg + w2] : mg;
-        }
-        Acc eg = 0, ntok = 0;
-        Acc acc[kSweeps][kVW];
+            mg = s_max[0];
 #pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw)
+            for (int w2 = 1; w2 < kMergeWarps; ++w2) mg = s_max[w2] > mg ? s_max[w2] : mg;
+            Acc eg, ntok;
+            Acc acc[kSweeps][kVW];
 #pragma unroll
-            for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
-        fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.c_stride, n, sub, wpg, mg, live, acc, eg, ntok, lane);
-        if (wpg > 1) {
+            for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+            fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.c_stride, n, warp, kMergeWarps, mg, live, acc, eg, ntok,
+                                               lane);
 #pragma unroll
             for (int sw = 0; sw < kSweeps; ++sw) {
                 const int j = sw * kPer + lane * kVW;
@@ -773,12 +824,13 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
                 s_tok[warp] = ntok;
             }
             __syncthreads();
-            if (sub == 0) {
+            if (warp == 0) {
                 eg = 0;
                 ntok = 0;
-                for (int w2 = 0; w2 < wpg; ++w2) {
-                    eg += s_e[slotw * wpg + w2];
-                    ntok += s_tok[slotw * wpg + w2];
+#pragma unroll
+                for (int w2 = 0; w2 < kMergeWarps; ++w2) {
+                    eg += s_e[w2];
+                    ntok += s_tok[w2];
                 }
 #pragma unroll
                 for (int sw = 0; sw < kSweeps; ++sw) {
@@ -787,31 +839,14 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
 #pragma unroll
                         for (int v = 0; v < kVW; ++v) {
                             Acc a = 0;
-                            for (int w2 = 0; w2 < wpg; ++w2) a += s_acc[slotw * wpg + w2][j + v];
+#pragma unroll
+                            for (int w2 = 0; w2 < kMergeWarps; ++w2) a += s_acc[w2][j + v];
                             acc[sw][v] = a;
                         }
                 }
+                push(g, acc, mg, eg, ntok);
             }
             __syncthreads();
-        }
-        if (gv && sub == 0) {
-            const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
-            for (int r = 0; r < x.nranks; ++r) {
-                Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
-#pragma unroll
-                for (int sw = 0; sw < kSweeps; ++sw) {
-                    const int j = sw * kPer + lane * kVW;
-                    if (j < DP)
-#pragma unroll
-                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
-                }
-                if (lane == 0) {
-                    dst[0] = ntok != Acc(0) ? mg : kNegInf;
-                    dst[1] = eg;
-                    dst[2] = ntok;
-                    dst[3] = 0;
-                }
-            }
         }
     }
     // ---- B. publish: one fence for the CTA, one flag per destination rank
