@@ -86,6 +86,8 @@ struct dattn_store {
     size_t staging_used = 0;
     unsigned long long work_base = 0;
     dattn::Plan scratch_plan;
+    std::vector<int32_t> last_words;  // plan currently in d_meta
+    bool meta_valid = false;
 
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
