@@ -113,7 +113,8 @@ typedef struct dattn_stats {
     int64_t last_items, last_chunks, last_plan_bytes;
     int32_t last_chunk_tokens, ma_grid;
     int32_t last_kernel;        /* 1: K1 CUDA-core MA, 2: K2 tcgen05 GQA MA */
-    int32_t last_exchange;      /* 1: NCCL allgather + K3, 2: fused K5 NVLink exchange */
+    int32_t last_exchange;      /* 0: fused merge inside K1 (1 GPU), 1: NCCL allgather + K3,
+                                   2: K5 NVLink exchange, 3: K1 group push + K6 rank merge */
     int64_t comm_timed;
     double comm_ms;             /* summed device time of the timed exchange (allgather or K5) */
 } dattn_stats;

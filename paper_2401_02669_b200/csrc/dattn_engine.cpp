@@ -100,7 +100,8 @@ void dattn_store::setup_exchange() {
     if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
     slot_stride = static_cast<int64_t>(cfg.max_seqs) * cfg.num_q_heads;
     const size_t xbytes = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
-    const size_t fbytes = static_cast<size_t>(nranks) * kMaxExchangeGrid * sizeof(uint32_t);
+    flag_stride = std::max<int64_t>(kMaxExchangeGrid, static_cast<int64_t>(cfg.max_seqs) * cfg.num_kv_heads);
+    const size_t fbytes = static_cast<size_t>(nranks) * flag_stride * sizeof(uint32_t);
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
     cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
@@ -373,6 +374,22 @@ void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl)
         any_kvh |= r.kv_head >= 0;
     }
     pl.any_kvh = any_kvh;
+    // chunk records per (row, kv head): the completion count of the fused merge
+    pl.off_expect = pl.words.size();
+    pl.words.resize(pl.off_expect + static_cast<size_t>(b.num_rows) * cfg.num_kv_heads, 0);
+    for (int i = 0; i < nr; ++i) {
+        const dattn_range& r = b.ranges[i];
+        const int64_t len = r.tok_end - r.tok_begin;
+        const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
+        int32_t* e = &pl.words[pl.off_expect + static_cast<size_t>(r.out_row) * cfg.num_kv_heads];
+        if (r.kv_head < 0)
+            for (int k = 0; k < cfg.num_kv_heads; ++k) e[k] += static_cast<int32_t>(nch);
+        else
+            e[r.kv_head] += static_cast<int32_t>(nch);
+    }
+    pl.any_empty_group = false;
+    for (size_t i = 0; i < static_cast<size_t>(b.num_rows) * cfg.num_kv_heads; ++i)
+        pl.any_empty_group |= pl.words[pl.off_expect + i] == 0;
     pl.nitems = static_cast<int32_t>(items);
     pl.nchunks = static_cast<int32_t>(one_chunk_per_range ? nr : chunks);
     pl.nranges = nr;
@@ -399,11 +416,35 @@ void dattn_store::upload_plan(const Plan& pl) {
     meta_valid = true;
 }
 
+// The fused group merge needs the K1 kernel (K2 keeps the separate merges)
+// and is switched off by DATTN_FUSED_K1=0.
+bool dattn_store::fused_ok(const Plan& pl, bool check_finite) const {
+    const char* env = std::getenv("DATTN_FUSED_K1");
+    if (env && std::atoi(env) == 0) return false;
+    (void)pl;  // rank-independent on purpose: every rank of a sharded step must agree
+    return !(tc_ok && !check_finite);
+}
+
+void dattn_store::fill_fused(const Plan& pl, MAParams& f) {
+    const size_t n = static_cast<size_t>(pl.nrows) * cfg.num_kv_heads;
+    if (n > gcounter_elems) {
+        gcounter.ensure(n * sizeof(int32_t));
+        cuda_check(cudaMemsetAsync(gcounter.p, 0, n * sizeof(int32_t), stream), "cudaMemsetAsync(counters)");
+        gcounter_elems = n;
+    }
+    const int32_t* w = static_cast<const int32_t*>(d_meta.p);
+    f.group_counter = static_cast<int32_t*>(gcounter.p);
+    f.group_expected = w + pl.off_expect;
+    f.row_begin = w + pl.off_rowchunk;
+    f.chunk_kvh = pl.any_kvh ? w + pl.off_kvh : nullptr;
+}
+
 void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double scale,
-                         bool check_finite) {
+                         bool check_finite, const MAParams* fused) {
     if (pl.nitems == 0) return;
     const int32_t* w = static_cast<const int32_t*>(d_meta.p);
     MAParams p{};
+    if (fused) p = *fused;
     p.k_pool = kpool;
     p.v_pool = vpool;
     p.block_tables = d_bt;
@@ -550,13 +591,28 @@ void dattn_store::decode(const dattn_batch& b, const void* q, void* out, void* r
     const bool check = (b.flags & DATTN_F_CHECK_FINITE) != 0;
     if (check) cuda_check(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), stream), "cudaMemsetAsync");
     recs.ensure(static_cast<size_t>(std::max(pl.nchunks, 1)) * cfg.num_q_heads * rec_bytes());
-    run_ma(pl, q_dev, recs.p, b.scale, check);
     void* out_dev = out;
     if (want_out && mem == DATTN_MEM_HOST) {
         obuf.ensure(q_bytes(b.num_rows));
         out_dev = obuf.p;
     }
-    local_merge(pl, recs.p, row_partials, want_out ? out_dev : nullptr);
+    // fused: the MA kernel merges each (row, kv head) group as it completes --
+    // no separate merge launch. Empty groups (no chunk) are never completed:
+    // zero their outputs up front; their identity records need the K3 path.
+    if (want_out && fused_ok(pl, check) && !(pl.any_empty_group && row_partials)) {
+        MAParams f{};
+        fill_fused(pl, f);
+        f.fused_mode = 1;
+        f.out_norm = out_dev;
+        f.out_recs = row_partials;
+        if (pl.any_empty_group)
+            cuda_check(cudaMemsetAsync(out_dev, 0, q_bytes(b.num_rows), stream), "cudaMemsetAsync(out)");
+        run_ma(pl, q_dev, recs.p, b.scale, check, &f);
+        stats.last_exchange = 0;
+    } else {
+        run_ma(pl, q_dev, recs.p, b.scale, check);
+        local_merge(pl, recs.p, row_partials, want_out ? out_dev : nullptr);
+    }
     if (mem == DATTN_MEM_HOST) {
         if (want_out)
             cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost,
@@ -597,13 +653,62 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         q_dev = qbuf.p;
     }
     recs.ensure(static_cast<size_t>(std::max(pl.nchunks, 1)) * cfg.num_q_heads * rec_bytes());
-    run_ma(pl, q_dev, recs.p, b.scale, false);
     const size_t row_recs = static_cast<size_t>(b.num_rows) * cfg.num_q_heads;
     void* out_dev0 = out;
     if (mem == DATTN_MEM_HOST) {
         obuf.ensure(q_bytes(b.num_rows));
         out_dev0 = obuf.p;
     }
+    if (fused_merge && static_cast<int64_t>(row_recs) <= slot_stride && fused_ok(pl, false)) {
+        // fused K1: every completed (row, kv head) group is merged and pushed to
+        // all ranks from inside the MA kernel, overlapping the exchange with the
+        // remaining streaming; K6 then merges the ranks' records.
+        MAParams f{};
+        fill_fused(pl, f);
+        f.fused_mode = 2;
+        for (int r = 0; r < nranks; ++r) {
+            f.peer_x[r] = peer_x[r];
+            f.peer_flags[r] = peer_flags[r];
+        }
+        f.rank = rank;
+        f.nranks = nranks;
+        f.slot_stride = slot_stride;
+        f.flag_stride = flag_stride;
+        f.epoch = ++epoch;
+        run_ma(pl, q_dev, recs.p, b.scale, false, &f);
+        RankMergeParams rp{};
+        rp.rows = b.num_rows;
+        rp.heads = cfg.num_q_heads;
+        rp.group = group;
+        rp.num_kv_heads = cfg.num_kv_heads;
+        rp.group_expected = static_cast<const int32_t*>(d_meta.p) + pl.off_expect;
+        for (int r = 0; r < nranks; ++r) {
+            rp.peer_x[r] = peer_x[r];
+            rp.peer_flags[r] = peer_flags[r];
+        }
+        rp.rank = rank;
+        rp.nranks = nranks;
+        rp.slot_stride = slot_stride;
+        rp.flag_stride = flag_stride;
+        rp.epoch = f.epoch;
+        rp.out_norm = out_dev0;
+        // all CTAs co-resident (<= 4 per SM): identity pushes precede every wait
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8, static_cast<int64_t>(num_sms) * 4)));
+        cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
+        if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
+        cuda_check(launch_rank_merge(cfg.dtype, dp, rp, grid, stream), "launch(K6 rank_merge)");
+        if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+        count_launch(1);
+        stats.last_exchange = 3;
+        if (mem == DATTN_MEM_HOST) {
+            cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost, stream),
+                       "cudaMemcpyAsync(out)");
+            cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+        }
+        return;
+    }
+    run_ma(pl, q_dev, recs.p, b.scale, false);
     if (fused_merge && static_cast<int64_t>(row_recs) <= slot_stride) {
         // K5: local merge + NVLink record exchange + rank merge in one launch
         const int32_t* w = static_cast<const int32_t*>(d_meta.p);
@@ -623,7 +728,7 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.rank = rank;
         xp.nranks = nranks;
         xp.slot_stride = slot_stride;
-        xp.flag_stride = kMaxExchangeGrid;
+        xp.flag_stride = flag_stride;
         xp.epoch = ++epoch;
         xp.out_norm = out_dev0;
         // 8 warps per group for long chunk lists, else one; the grid depends

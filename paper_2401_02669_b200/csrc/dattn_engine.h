@@ -48,9 +48,10 @@ struct HostBuf {
 // Decode plan: the int32 metadata block uploaded once per call.
 struct Plan {
     std::vector<int32_t> words;
-    size_t off_ranges = 0, off_item = 0, off_chunk = 0, off_rowchunk = 0, off_kvh = 0;
+    size_t off_ranges = 0, off_item = 0, off_chunk = 0, off_rowchunk = 0, off_kvh = 0, off_expect = 0;
     int32_t nitems = 0, nchunks = 0, nranges = 0, nrows = 0, chunk_tokens = 0;
     bool any_kvh = false;
+    bool any_empty_group = false;  // some (row, kv head) has no chunk on this store
 };
 
 }  // namespace dattn
@@ -97,6 +98,7 @@ struct dattn_store {
     void* peer_x[8]{};
     uint32_t* peer_flags[8]{};
     int64_t slot_stride = 0;
+    int64_t flag_stride = 0;
     uint32_t epoch = 0;
     bool fused_merge = false;
     void setup_exchange();
@@ -127,7 +129,11 @@ struct dattn_store {
     void plan(const dattn_batch& b, bool one_chunk_per_range, dattn::Plan& pl) const;
     void upload_plan(const dattn::Plan& pl);
     void run_ma(const dattn::Plan& pl, const void* q_dev, void* recs, double scale,
-                bool check_finite);
+                bool check_finite, const dattn::MAParams* fused = nullptr);
+    bool fused_ok(const dattn::Plan& pl, bool check_finite) const;
+    void fill_fused(const dattn::Plan& pl, dattn::MAParams& f);
+    dattn::DevBuf gcounter;
+    size_t gcounter_elems = 0;
     void run_merge(const dattn::MergeParams& mp);
     void local_merge(const dattn::Plan& pl, const void* recs, void* out_recs, void* out_norm);
     void check_flag();

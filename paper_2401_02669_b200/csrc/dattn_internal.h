@@ -39,6 +39,42 @@ struct MAParams {
     unsigned long long work_base;      // counter value at this launch's start
     int32_t* nonfinite_flag;  // may be null
     int32_t stages;
+    // ---- fused group merge (K1 only; fused_mode 0 = records only) ----
+    // 1: the CTA completing the last chunk of a (row, kv head) group merges the
+    //    group's records into out_norm (and out_recs if set);
+    // 2: ... and pushes the merged records to every rank's exchange buffer,
+    //    then raises the group's flag on every rank (rank merge: K6).
+    int32_t fused_mode;
+    int32_t* group_counter;          // [rows][Hkv], self-resetting
+    const int32_t* group_expected;   // [rows][Hkv] chunk records per group
+    const int32_t* row_begin;        // [rows+1] first chunk of every row
+    const int32_t* chunk_kvh;        // per chunk kv-head tag (-1 all) or null
+    void* out_norm;                  // [rows][Hq][DP] storage dtype
+    void* out_recs;                  // [rows][Hq][DP+4] or null
+    void* peer_x[8];
+    uint32_t* peer_flags[8];
+    int32_t rank;
+    int32_t nranks;
+    int64_t slot_stride;             // records per source rank
+    int64_t flag_stride;             // flags per source rank
+    uint32_t epoch;
+};
+
+// K6: rank merge after fused K1 (waits for every rank's group flags).
+struct RankMergeParams {
+    int32_t rows;
+    int32_t heads;
+    int32_t group;
+    int32_t num_kv_heads;
+    const int32_t* group_expected;   // this rank's [rows][Hkv]: 0 -> push identity
+    void* peer_x[8];
+    uint32_t* peer_flags[8];
+    int32_t rank;
+    int32_t nranks;
+    int64_t slot_stride;
+    int64_t flag_stride;
+    uint32_t epoch;
+    void* out_norm;
 };
 
 // K3 merge launch.
@@ -138,6 +174,7 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
                       cudaStream_t st);
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st);
+cudaError_t launch_rank_merge(int dtype, int dp, const RankMergeParams& p, int grid, cudaStream_t st);
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st);
 cudaError_t launch_append(int dtype, int dp, const AppendParams& p, cudaStream_t st);
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);

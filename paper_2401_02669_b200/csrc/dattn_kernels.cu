@@ -121,6 +121,215 @@ __device__ __forceinline__ int find_range(const int32_t* prefix, int n, int item
     return lo;
 }
 
+constexpr int kMergeWarps = 8;
+
+// Rescale-sum of the live chunk records c = sub + stride*i (< n) of one group:
+// lanes first compute the weights w = exp(m - m_g) of 32 records in parallel,
+// then the warp folds the records' ma vectors (lane-owned kVW-element slices,
+// independent vector loads) with the broadcast weights. Dead records get
+// w = 0; identity records hold ma = 0, so adding them changes nothing and a
+// single live record is reproduced exactly. Returns warp-reduced (e, tokens).
+template <typename Acc, int DP, int kVW, int kSweeps, typename LiveF>
+__device__ __forceinline__ void fold_chunks(const Acc* R, int64_t base, int64_t c_stride, int n, int sub,
+                                            int stride, Acc mg, LiveF live, Acc (&acc)[kSweeps][kVW],
+                                            Acc& eg, Acc& ntok, int lane) {
+    constexpr int REC = DP + 4;
+    constexpr int kPer = 32 * kVW;
+    Acc e_l = 0, t_l = 0;
+    for (int i0 = 0; sub + stride * i0 < n; i0 += 32) {
+        const int c = sub + stride * (i0 + lane);
+        Acc w = 0;
+        if (c < n) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * c_stride) * REC;
+            if (live(c, r)) {
+                const Acc mc = __ldcg(r);
+                w = (mc == mg) ? Acc(1) : exp(mc - mg);
+                e_l += __ldcg(r + 1) * w;
+                t_l += __ldcg(r + 2);
+            }
+        }
+        const int cnt = min(32, (n - sub - stride * i0 + stride - 1) / stride);
+#pragma unroll 4
+        for (int k = 0; k < cnt; ++k) {
+            const Acc wk = __shfl_sync(0xffffffffu, w, k);
+            const Acc* r = R + (base + static_cast<int64_t>(sub + stride * (i0 + k)) * c_stride) * REC;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP) {
+                    if constexpr (kVW == 4) {
+                        const float4 x = __ldcg(reinterpret_cast<const float4*>(r + 4 + j));
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                        acc[sw][2] += x.z * wk; acc[sw][3] += x.w * wk;
+                    } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
+                        const double2 x = __ldcg(reinterpret_cast<const double2*>(r + 4 + j));
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) acc[sw][v] += __ldcg(r + 4 + j + v) * wk;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        e_l += __shfl_xor_sync(0xffffffffu, e_l, off);
+        t_l += __shfl_xor_sync(0xffffffffu, t_l, off);
+    }
+    eg = e_l;
+    ntok = t_l;
+}
+
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Fused group merge (run by the 8 consumer warps of the CTA that completed the
+// last chunk of (row, kvh)): for every q head of the kv head, rescale-sum the
+// row's chunk records (aggregate_partials, distattention.cpp:150-174), then
+// write the normalised output (mode 1) or push the merged record to every
+// rank's exchange buffer and raise the group's flag there (mode 2).
+template <typename T, int DP>
+__device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, int lane,
+                                  typename Elem<T>::Acc* red_m, typename Elem<T>::Acc* red_e,
+                                  typename Elem<T>::Acc* red_acc) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int REC = DP + 4;
+    constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
+                                           : (DP % 64 == 0 ? 2 : 1);
+    constexpr int kPer = 32 * kVW;
+    constexpr int kSweeps = (DP + kPer - 1) / kPer;
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    const int G = p.group;
+    const int hpass = G < kConsumerWarps ? G : kConsumerWarps;  // heads per pass
+    const int wph2 = kConsumerWarps / hpass;                      // warps per head
+    const int cbase = p.row_begin[row];
+    const int n = p.row_begin[row + 1] - cbase;
+    const Acc* R = static_cast<const Acc*>(p.records);
+    __shared__ Acc s_tok[kConsumerWarps];
+    for (int hh0 = 0; hh0 < G; hh0 += hpass) {
+        const int slot = cw / wph2, sub = cw - slot * wph2;
+        const int hh = hh0 + slot;
+        const bool hv = slot < hpass && hh < G;
+        const int h = kvh * G + (hv ? hh : 0);
+        const int64_t base = static_cast<int64_t>(cbase) * p.num_q_heads + h;
+        auto live = [&](int c, const Acc* r) {
+            if (p.chunk_kvh) {
+                const int tag = p.chunk_kvh[cbase + c];
+                if (tag >= 0 && tag != kvh) return false;
+            }
+            return __ldcg(r + 2) != Acc(0);
+        };
+        Acc mg = kNegInf;
+        if (hv)
+            for (int c = sub * 32 + lane; c < n; c += wph2 * 32) {
+                const Acc* r = R + (base + static_cast<int64_t>(c) * p.num_q_heads) * REC;
+                if (live(c, r)) {
+                    const Acc mc = __ldcg(r);
+                    mg = mc > mg ? mc : mg;
+                }
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+            mg = o > mg ? o : mg;
+        }
+        if (lane == 0) red_m[cw] = mg;
+        named_bar_sync(1, 32 * kConsumerWarps);
+        mg = kNegInf;
+        for (int w2 = 0; w2 < wph2; ++w2) {
+            const Acc mm = red_m[slot * wph2 + w2];
+            mg = mm > mg ? mm : mg;
+        }
+        Acc eg = 0, ntok = 0;
+        Acc acc[kSweeps][kVW];
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+        if (hv) fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.num_q_heads, n, sub, wph2, mg, live, acc, eg, ntok, lane);
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw) {
+            const int j = sw * kPer + lane * kVW;
+            if (j < DP)
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) red_acc[cw * DP + j + v] = acc[sw][v];
+        }
+        if (lane == 0) {
+            red_e[cw] = eg;
+            s_tok[cw] = ntok;
+        }
+        named_bar_sync(1, 32 * kConsumerWarps);
+        if (hv && sub == 0) {
+            eg = 0;
+            ntok = 0;
+            for (int w2 = 0; w2 < wph2; ++w2) {
+                eg += red_e[slot * wph2 + w2];
+                ntok += s_tok[slot * wph2 + w2];
+            }
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) {
+                        Acc a = 0;
+                        for (int w2 = 0; w2 < wph2; ++w2) a += red_acc[(slot * wph2 + w2) * DP + j + v];
+                        acc[sw][v] = a;
+                    }
+            }
+            const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + h;
+            if (p.fused_mode == 1) {
+                T* o = static_cast<T*>(p.out_norm) + g * DP;
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v)
+                            o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
+                }
+            }
+            Acc* dsts[8];
+            int nd = 0;
+            if (p.fused_mode == 1 && p.out_recs) dsts[nd++] = static_cast<Acc*>(p.out_recs) + g * REC;
+            if (p.fused_mode == 2)
+                for (int r = 0; r < p.nranks; ++r)
+                    dsts[nd++] = static_cast<Acc*>(p.peer_x[r]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC;
+            for (int d = 0; d < nd; ++d) {
+                Acc* dst = dsts[d];
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+                }
+                if (lane == 0) {
+                    dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                    dst[1] = eg;
+                    dst[2] = ntok;
+                    dst[3] = 0;
+                }
+            }
+        }
+        named_bar_sync(1, 32 * kConsumerWarps);
+    }
+    if (p.fused_mode == 2 && cw == 0 && lane == 0) {
+        __threadfence_system();
+        const int64_t f = static_cast<int64_t>(p.rank) * p.flag_stride + static_cast<int64_t>(row) * p.num_kv_heads + kvh;
+        for (int r = 0; r < p.nranks; ++r) st_release_sys(p.peer_flags[r] + f, p.epoch);
+    }
+}
+
 template <typename T, int DP, int HPW>
 __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 2)
     ma_decode_kernel(const MAParams p) {
@@ -488,6 +697,25 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                 }
                 named_bar_sync(1, 32 * kConsumerWarps);
             }
+            if (p.fused_mode != 0) {
+                // ---- group completion: the CTA that wrote the last chunk of
+                //      (row, kv head) merges the group (threadfence pattern)
+                __shared__ int s_last;
+                named_bar_sync(1, 32 * kConsumerWarps);  // this item's records are issued
+                if (cw == 0 && lane == 0) {
+                    __threadfence();
+                    const int gi = md.row * p.num_kv_heads + md.kvh;
+                    const int old = atomicAdd(p.group_counter + gi, 1);
+                    const int last = (old + 1 == __ldg(p.group_expected + gi)) ? 1 : 0;
+                    if (last) p.group_counter[gi] = 0;  // ready for the next launch
+                    s_last = last;
+                }
+                named_bar_sync(1, 32 * kConsumerWarps);
+                if (s_last) {
+                    __threadfence();
+                    fused_group_merge<T, DP>(p, md.row, md.kvh, cw, lane, red_m, red_e, red_acc);
+                }
+            }
         }
         if (++stage == stages) {
             stage = 0;
@@ -502,64 +730,6 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
 // records. Pass 2: warp w folds records w, w+8, ... with vector loads (each
 // lane owns kVW contiguous elements of ma), then the 8 warp partials are
 // summed through shared memory in a fixed order (deterministic).
-constexpr int kMergeWarps = 8;
-
-// Rescale-sum of the live chunk records c = sub + stride*i (< n) of one group:
-// lanes first compute the weights w = exp(m - m_g) of 32 records in parallel,
-// then the warp folds the records' ma vectors (lane-owned kVW-element slices,
-// independent vector loads) with the broadcast weights. Dead records get
-// w = 0; identity records hold ma = 0, so adding them changes nothing and a
-// single live record is reproduced exactly. Returns warp-reduced (e, tokens).
-template <typename Acc, int DP, int kVW, int kSweeps, typename LiveF>
-__device__ __forceinline__ void fold_chunks(const Acc* R, int64_t base, int64_t c_stride, int n, int sub,
-                                            int stride, Acc mg, LiveF live, Acc (&acc)[kSweeps][kVW],
-                                            Acc& eg, Acc& ntok, int lane) {
-    constexpr int REC = DP + 4;
-    constexpr int kPer = 32 * kVW;
-    Acc e_l = 0, t_l = 0;
-    for (int i0 = 0; sub + stride * i0 < n; i0 += 32) {
-        const int c = sub + stride * (i0 + lane);
-        Acc w = 0;
-        if (c < n) {
-            const Acc* r = R + (base + static_cast<int64_t>(c) * c_stride) * REC;
-            if (live(c, r)) {
-                w = (r[0] == mg) ? Acc(1) : exp(r[0] - mg);
-                e_l += r[1] * w;
-                t_l += r[2];
-            }
-        }
-        const int cnt = min(32, (n - sub - stride * i0 + stride - 1) / stride);
-#pragma unroll 4
-        for (int k = 0; k < cnt; ++k) {
-            const Acc wk = __shfl_sync(0xffffffffu, w, k);
-            const Acc* r = R + (base + static_cast<int64_t>(sub + stride * (i0 + k)) * c_stride) * REC;
-#pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP) {
-                    if constexpr (kVW == 4) {
-                        const float4 x = *reinterpret_cast<const float4*>(r + 4 + j);
-                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
-                        acc[sw][2] += x.z * wk; acc[sw][3] += x.w * wk;
-                    } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
-                        const double2 x = *reinterpret_cast<const double2*>(r + 4 + j);
-                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < kVW; ++v) acc[sw][v] += r[4 + j + v] * wk;
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        e_l += __shfl_xor_sync(0xffffffffu, e_l, off);
-        t_l += __shfl_xor_sync(0xffffffffu, t_l, off);
-    }
-    eg = e_l;
-    ntok = t_l;
-}
 
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergeParams p) {
@@ -668,14 +838,6 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
 // it with a release store of the step epoch into the owner's flag, waits for
 // the flags of all ranks (acquire, system scope) and merges the nranks records
 // into the output. Replaces local K3 + ncclAllGather + rank K3.
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // A CTA owns groups [(blockIdx.x + k*gridDim.x)*gpc, +gpc) with gpc = 8/wpg
 // groups per iteration and wpg warps per group (1 for short chunk lists, 8
@@ -914,6 +1076,91 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             if (j < DP)
 #pragma unroll
                 for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(tok2 != Acc(0) ? a2[sw][v] / e2 : Acc(0));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K6
+// Rank merge after the fused K1: one warp per (row, q head). This rank first
+// publishes identity records for its groups that hold no tokens (no K1 CTA
+// completes them), then every warp waits for its group's flag from every
+// rank and merges the nranks records into the output. CTAs never wait for
+// each other on this GPU; peers' flags come from their K1 or K6.
+template <typename T, int DP>
+__global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const RankMergeParams x) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int REC = DP + 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    const int64_t ngroups_kv = static_cast<int64_t>(x.rows) * x.num_kv_heads;
+    // identity records for empty (row, kv head) groups of this rank
+    for (int64_t gk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gk < ngroups_kv;
+         gk += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (x.group_expected[gk] != 0) continue;
+        const int row = static_cast<int>(gk / x.num_kv_heads), kvh = static_cast<int>(gk % x.num_kv_heads);
+        for (int hh = 0; hh < x.group; ++hh) {
+            const int64_t g = static_cast<int64_t>(row) * x.heads + kvh * x.group + hh;
+            for (int r = 0; r < x.nranks; ++r) {
+                Acc* dst = static_cast<Acc*>(x.peer_x[r]) + (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
+                dst[0] = kNegInf;
+                dst[1] = 0;
+                dst[2] = 0;
+                dst[3] = 0;  // ma is never read for identity records
+            }
+        }
+        __threadfence_system();
+        for (int r = 0; r < x.nranks; ++r)
+            st_release_sys(x.peer_flags[r] + static_cast<int64_t>(x.rank) * x.flag_stride + gk, x.epoch);
+    }
+    const int64_t groups = static_cast<int64_t>(x.rows) * x.heads;
+    const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
+         g += static_cast<int64_t>(gridDim.x) * kMergeWarps) {
+        const int row = static_cast<int>(g / x.heads);
+        const int h = static_cast<int>(g - static_cast<int64_t>(row) * x.heads);
+        const int64_t gk = static_cast<int64_t>(row) * x.num_kv_heads + h / x.group;
+        if (lane < x.nranks) {
+            const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(lane) * x.flag_stride + gk;
+            uint64_t t0 = 0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (ld_acquire_sys(f) != x.epoch) {
+                __nanosleep(32);
+                uint64_t t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                if (t1 - t0 > 10000000000ull) __trap();
+            }
+        }
+        __syncwarp();
+        Acc m2 = kNegInf;
+        for (int r = 0; r < x.nranks; ++r) {
+            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
+        }
+        Acc e2 = 0, tok2 = 0;
+        constexpr int EPL = (DP + 31) / 32;
+        Acc a2[EPL];
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) a2[k] = 0;
+        for (int r = 0; r < x.nranks; ++r) {
+            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            const Acc tk = __ldcv(rec + 2);
+            if (tk == Acc(0)) continue;
+            const Acc mr = __ldcv(rec);
+            const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
+            e2 += __ldcv(rec + 1) * w;
+            tok2 += tk;
+#pragma unroll
+            for (int k = 0; k < EPL; ++k) {
+                const int j = lane + 32 * k;
+                if (j < DP) a2[k] += __ldcv(rec + 4 + j) * w;
+            }
+        }
+        T* o = static_cast<T*>(x.out_norm) + g * DP;
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+            const int j = lane + 32 * k;
+            if (j < DP) o[j] = E::from_acc(tok2 != Acc(0) ? a2[k] / e2 : Acc(0));
         }
     }
 }
@@ -1162,6 +1409,11 @@ static int grid_for(int64_t total) {
 
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st) {
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_exchange_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rank_merge(int dtype, int dp, const RankMergeParams& p, int grid, cudaStream_t st) {
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (rank_merge_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
     return cudaGetLastError();
 }
 
