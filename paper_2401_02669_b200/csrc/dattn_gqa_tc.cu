@@ -27,6 +27,7 @@
 
 #include "dattn_internal.h"
 #include "dattn_ptx.cuh"
+#include "dattn_merge.cuh"
 
 namespace dattn {
 namespace tc {
@@ -70,6 +71,8 @@ struct Smem {
     int32_t pid[kPidWin];
     float red_max[2][4][kN];
     float red_sum[4][kN];
+    float mrg_m[4], mrg_e[4], mrg_acc[4 * kD];  // fused group merge scratch
+    int32_t s_last;
     uint32_t tmem_base;
 };
 
@@ -511,6 +514,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 named_bar_sync(1, 128);
+                if (p.fused_mode != 0) {
+                    // group completion (see K1): the CTA that wrote the last
+                    // chunk of (row, kv head) merges the group
+                    if (warp == 2 && lane == 0) {
+                        __threadfence();
+                        const int gi = md.row * p.num_kv_heads + md.kvh;
+                        const int old = atomicAdd(p.group_counter + gi, 1);
+                        const int last = (old + 1 == __ldg(p.group_expected + gi)) ? 1 : 0;
+                        if (last) p.group_counter[gi] = 0;
+                        S.s_last = last;
+                    }
+                    named_bar_sync(1, 128);
+                    if (S.s_last) {
+                        __threadfence();
+                        fused_group_merge<bf16_t, kD, 4>(p, md.row, md.kvh, warp - 2, lane, S.mrg_m, S.mrg_e,
+                                                          S.mrg_acc);
+                    }
+                    named_bar_sync(1, 128);
+                }
             }
         }
     }

@@ -1,0 +1,226 @@
+// dattn_merge.cuh -- device-side partial-record merging shared by the MA
+// kernels (fused group merge) and the merge kernels (K3, K5, K6):
+// the online-softmax rescale-and-sum of aggregate_partials /
+// combine_partials (/root/reference/proj/src/distattention.cpp:131-174).
+#pragma once
+#include <cmath>
+#include <cstdint>
+
+#include "dattn_internal.h"
+#include "dattn_ptx.cuh"
+
+namespace dattn {
+
+constexpr int kConsumerWarps = 8;
+
+constexpr int kMergeWarps = 8;
+
+// Rescale-sum of the live chunk records c = sub + stride*i (< n) of one group:
+// lanes first compute the weights w = exp(m - m_g) of 32 records in parallel,
+// then the warp folds the records' ma vectors (lane-owned kVW-element slices,
+// independent vector loads) with the broadcast weights. Dead records get
+// w = 0; identity records hold ma = 0, so adding them changes nothing and a
+// single live record is reproduced exactly. Returns warp-reduced (e, tokens).
+template <typename Acc, int DP, int kVW, int kSweeps, typename LiveF>
+__device__ __forceinline__ void fold_chunks(const Acc* R, int64_t base, int64_t c_stride, int n, int sub,
+                                            int stride, Acc mg, LiveF live, Acc (&acc)[kSweeps][kVW],
+                                            Acc& eg, Acc& ntok, int lane) {
+    constexpr int REC = DP + 4;
+    constexpr int kPer = 32 * kVW;
+    Acc e_l = 0, t_l = 0;
+    for (int i0 = 0; sub + stride * i0 < n; i0 += 32) {
+        const int c = sub + stride * (i0 + lane);
+        Acc w = 0;
+        if (c < n) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * c_stride) * REC;
+            if (live(c, r)) {
+                const Acc mc = __ldcg(r);
+                w = (mc == mg) ? Acc(1) : exp(mc - mg);
+                e_l += __ldcg(r + 1) * w;
+                t_l += __ldcg(r + 2);
+            }
+        }
+        const int cnt = min(32, (n - sub - stride * i0 + stride - 1) / stride);
+#pragma unroll 4
+        for (int k = 0; k < cnt; ++k) {
+            const Acc wk = __shfl_sync(0xffffffffu, w, k);
+            const Acc* r = R + (base + static_cast<int64_t>(sub + stride * (i0 + k)) * c_stride) * REC;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP) {
+                    if constexpr (kVW == 4) {
+                        const float4 x = __ldcg(reinterpret_cast<const float4*>(r + 4 + j));
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                        acc[sw][2] += x.z * wk; acc[sw][3] += x.w * wk;
+                    } else if constexpr (kVW == 2 && sizeof(Acc) == 8) {
+                        const double2 x = __ldcg(reinterpret_cast<const double2*>(r + 4 + j));
+                        acc[sw][0] += x.x * wk; acc[sw][1] += x.y * wk;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) acc[sw][v] += __ldcg(r + 4 + j + v) * wk;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        e_l += __shfl_xor_sync(0xffffffffu, e_l, off);
+        t_l += __shfl_xor_sync(0xffffffffu, t_l, off);
+    }
+    eg = e_l;
+    ntok = t_l;
+}
+
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Fused group merge (run by the 8 consumer warps of the CTA that completed the
+// last chunk of (row, kvh)): for every q head of the kv head, rescale-sum the
+// row's chunk records (aggregate_partials, distattention.cpp:150-174), then
+// write the normalised output (mode 1) or push the merged record to every
+// rank's exchange buffer and raise the group's flag there (mode 2).
+template <typename T, int DP, int NW = kConsumerWarps>
+__device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, int lane,
+                                  typename Elem<T>::Acc* red_m, typename Elem<T>::Acc* red_e,
+                                  typename Elem<T>::Acc* red_acc) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int REC = DP + 4;
+    constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
+                                           : (DP % 64 == 0 ? 2 : 1);
+    constexpr int kPer = 32 * kVW;
+    constexpr int kSweeps = (DP + kPer - 1) / kPer;
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    const int G = p.group;
+    const int hpass = G < NW ? G : NW;  // heads per pass
+    const int wph2 = NW / hpass;                      // warps per head
+    const int cbase = p.row_begin[row];
+    const int n = p.row_begin[row + 1] - cbase;
+    const Acc* R = static_cast<const Acc*>(p.records);
+    __shared__ Acc s_tok[NW];
+    for (int hh0 = 0; hh0 < G; hh0 += hpass) {
+        const int slot = cw / wph2, sub = cw - slot * wph2;
+        const int hh = hh0 + slot;
+        const bool hv = slot < hpass && hh < G;
+        const int h = kvh * G + (hv ? hh : 0);
+        const int64_t base = static_cast<int64_t>(cbase) * p.num_q_heads + h;
+        auto live = [&](int c, const Acc* r) {
+            if (p.chunk_kvh) {
+                const int tag = p.chunk_kvh[cbase + c];
+                if (tag >= 0 && tag != kvh) return false;
+            }
+            return __ldcg(r + 2) != Acc(0);
+        };
+        Acc mg = kNegInf;
+        if (hv)
+            for (int c = sub * 32 + lane; c < n; c += wph2 * 32) {
+                const Acc* r = R + (base + static_cast<int64_t>(c) * p.num_q_heads) * REC;
+                if (live(c, r)) {
+                    const Acc mc = __ldcg(r);
+                    mg = mc > mg ? mc : mg;
+                }
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+            mg = o > mg ? o : mg;
+        }
+        if (lane == 0) red_m[cw] = mg;
+        named_bar_sync(1, 32 * NW);
+        mg = kNegInf;
+        for (int w2 = 0; w2 < wph2; ++w2) {
+            const Acc mm = red_m[slot * wph2 + w2];
+            mg = mm > mg ? mm : mg;
+        }
+        Acc eg = 0, ntok = 0;
+        Acc acc[kSweeps][kVW];
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+        if (hv) fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.num_q_heads, n, sub, wph2, mg, live, acc, eg, ntok, lane);
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw) {
+            const int j = sw * kPer + lane * kVW;
+            if (j < DP)
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) red_acc[cw * DP + j + v] = acc[sw][v];
+        }
+        if (lane == 0) {
+            red_e[cw] = eg;
+            s_tok[cw] = ntok;
+        }
+        named_bar_sync(1, 32 * NW);
+        if (hv && sub == 0) {
+            eg = 0;
+            ntok = 0;
+            for (int w2 = 0; w2 < wph2; ++w2) {
+                eg += red_e[slot * wph2 + w2];
+                ntok += s_tok[slot * wph2 + w2];
+            }
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) {
+                        Acc a = 0;
+                        for (int w2 = 0; w2 < wph2; ++w2) a += red_acc[(slot * wph2 + w2) * DP + j + v];
+                        acc[sw][v] = a;
+                    }
+            }
+            const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + h;
+            if (p.fused_mode == 1) {
+                T* o = static_cast<T*>(p.out_norm) + g * DP;
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v)
+                            o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
+                }
+            }
+            Acc* dsts[8];
+            int nd = 0;
+            if (p.fused_mode == 1 && p.out_recs) dsts[nd++] = static_cast<Acc*>(p.out_recs) + g * REC;
+            if (p.fused_mode == 2)
+                for (int r = 0; r < p.nranks; ++r)
+                    dsts[nd++] = static_cast<Acc*>(p.peer_x[r]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC;
+            for (int d = 0; d < nd; ++d) {
+                Acc* dst = dsts[d];
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+                }
+                if (lane == 0) {
+                    dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                    dst[1] = eg;
+                    dst[2] = ntok;
+                    dst[3] = 0;
+                }
+            }
+        }
+        named_bar_sync(1, 32 * NW);
+    }
+    if (p.fused_mode == 2 && cw == 0 && lane == 0) {
+        __threadfence_system();
+        const int64_t f = static_cast<int64_t>(p.rank) * p.flag_stride + static_cast<int64_t>(row) * p.num_kv_heads + kvh;
+        for (int r = 0; r < p.nranks; ++r) st_release_sys(p.peer_flags[r] + f, p.epoch);
+    }
+}
+
+
+}  // namespace dattn
