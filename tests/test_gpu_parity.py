@@ -239,6 +239,31 @@ def test_gqa_tcgen05_path_vs_oracle_and_cuda_core_path(torch_cuda, group, lens):
     assert rel_errs(outk[:1], ref[:1]) < 2e-2
 
 
+@pytest.mark.parametrize("hq,hkv", [(32, 32), (64, 8)])
+def test_fused_group_merge_equals_separate_merge(torch_cuda, hq, hkv):
+    """The in-kernel group merge (completion counters, K1 and K2) and the
+    separate K3 merge launch give the same outputs (to fp32 re-association)."""
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    lens = [5000, 1, 17, 2048, 9999, 64]
+    st, seqs, q = make(torch, lens, hq, hkv, 128, pb.BF16, seed=12, rows=7)
+    rg = []
+    for b, (s, L) in enumerate(zip(seqs, lens)):
+        rg += [pb.Range(s, b, 0, L // 3), pb.Range(s, b, L // 3, L)]
+    fused = out_np(torch, decode(torch, st, rg, 7, q), 128)
+    assert st.stats().last_exchange == 0
+    os.environ["DATTN_FUSED_K1"] = "0"
+    try:
+        sep = out_np(torch, decode(torch, st, rg, 7, q), 128)
+    finally:
+        del os.environ["DATTN_FUSED_K1"]
+    assert rel_errs(fused[:6], sep[:6]) < 1e-5
+    assert not fused[6].any() and not sep[6].any()  # row without ranges
+    # repeated launches reuse the self-resetting completion counters
+    again = out_np(torch, decode(torch, st, rg, 7, q), 128)
+    assert np.array_equal(again, fused)
+
+
 def test_adversarial_logits_and_partition_invariance(torch_cuda):
     """Key amplitude 30 (verify.cpp:90) forces large max shifts across chunks;
     any chunking / rBlock cut gives the same output."""
