@@ -99,9 +99,13 @@ void dattn_store::setup_exchange() {
     const char* env = std::getenv("DATTN_FUSED_MERGE");
     if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
     slot_stride = static_cast<int64_t>(cfg.max_seqs) * cfg.num_q_heads;
-    const size_t xbytes = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
+    // two halves, used by alternate steps (epoch parity): a rank that runs one
+    // step ahead never overwrites records or flags a slower peer still reads
+    xhalf = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
+    const size_t xbytes = 2 * xhalf;
     flag_stride = std::max<int64_t>(kMaxExchangeGrid, static_cast<int64_t>(cfg.max_seqs) * cfg.num_kv_heads);
-    const size_t fbytes = static_cast<size_t>(nranks) * flag_stride * sizeof(uint32_t);
+    fhalf = static_cast<size_t>(nranks) * flag_stride;
+    const size_t fbytes = 2 * fhalf * sizeof(uint32_t);
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
     cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
@@ -667,15 +671,15 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         MAParams f{};
         fill_fused(pl, f);
         f.fused_mode = 2;
+        f.epoch = ++epoch;
         for (int r = 0; r < nranks; ++r) {
-            f.peer_x[r] = peer_x[r];
-            f.peer_flags[r] = peer_flags[r];
+            f.peer_x[r] = xhalf_ptr(peer_x[r], f.epoch);
+            f.peer_flags[r] = fhalf_ptr(peer_flags[r], f.epoch);
         }
         f.rank = rank;
         f.nranks = nranks;
         f.slot_stride = slot_stride;
         f.flag_stride = flag_stride;
-        f.epoch = ++epoch;
         run_ma(pl, q_dev, recs.p, b.scale, false, &f);
         RankMergeParams rp{};
         rp.rows = b.num_rows;
@@ -684,8 +688,8 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         rp.num_kv_heads = cfg.num_kv_heads;
         rp.group_expected = static_cast<const int32_t*>(d_meta.p) + pl.off_expect;
         for (int r = 0; r < nranks; ++r) {
-            rp.peer_x[r] = peer_x[r];
-            rp.peer_flags[r] = peer_flags[r];
+            rp.peer_x[r] = f.peer_x[r];
+            rp.peer_flags[r] = f.peer_flags[r];
         }
         rp.rank = rank;
         rp.nranks = nranks;
@@ -722,15 +726,15 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.local.c_stride = cfg.num_q_heads;
         xp.local.chunk_kvh = pl.any_kvh ? w + pl.off_kvh : nullptr;
         xp.local.group = group;
+        xp.epoch = ++epoch;
         for (int r = 0; r < nranks; ++r) {
-            xp.peer_x[r] = peer_x[r];
-            xp.peer_flags[r] = peer_flags[r];
+            xp.peer_x[r] = xhalf_ptr(peer_x[r], xp.epoch);
+            xp.peer_flags[r] = fhalf_ptr(peer_flags[r], xp.epoch);
         }
         xp.rank = rank;
         xp.nranks = nranks;
         xp.slot_stride = slot_stride;
         xp.flag_stride = flag_stride;
-        xp.epoch = ++epoch;
         xp.out_norm = out_dev0;
         // 8 warps per group for long chunk lists, else one; the grid depends
         // only on the row count and chunk shape, identical on every rank, and

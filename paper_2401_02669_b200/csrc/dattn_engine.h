@@ -99,6 +99,11 @@ struct dattn_store {
     uint32_t* peer_flags[8]{};
     int64_t slot_stride = 0;
     int64_t flag_stride = 0;
+    size_t xhalf = 0, fhalf = 0;  // bytes / flags of one exchange half
+    void* xhalf_ptr(void* base, uint32_t ep) const {
+        return static_cast<unsigned char*>(base) + (ep & 1u) * xhalf;
+    }
+    uint32_t* fhalf_ptr(uint32_t* base, uint32_t ep) const { return base + (ep & 1u) * fhalf; }
     uint32_t epoch = 0;
     bool fused_merge = false;
     void setup_exchange();

@@ -75,9 +75,11 @@ def _worker(rank, world, port, case, placement, fused, q):
         st.comm_init(uid[0], rank, world)
         st.decode_sharded(ranges, len(lens), qd, out)
         torch.cuda.synchronize()
-        assert st.stats().last_exchange == (2 if fused else 1)
-        # repeated steps reuse the exchange buffers (epoch flags)
-        for _ in range(3):
+        # fused: MA kernels push merged groups over NVLink (3) / K5 (2)
+        assert st.stats().last_exchange in ((2, 3) if fused else (1,))
+        # repeated back-to-back steps reuse the double-buffered exchange
+        # (epoch flags): ranks may run a step ahead of each other
+        for _ in range(20):
             st.decode_sharded(ranges, len(lens), qd, out)
         torch.cuda.synchronize()
         # host-memory path gives the same bytes
