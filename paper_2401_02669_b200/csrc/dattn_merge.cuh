@@ -190,14 +190,12 @@ __device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, i
                             o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
                 }
             }
-            Acc* dsts[8];
-            int nd = 0;
-            if (p.fused_mode == 1 && p.out_recs) dsts[nd++] = static_cast<Acc*>(p.out_recs) + g * REC;
-            if (p.fused_mode == 2)
-                for (int r = 0; r < p.nranks; ++r)
-                    dsts[nd++] = static_cast<Acc*>(p.peer_x[r]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC;
+            // merged record -> out_recs (mode 1) or every rank's exchange slot (mode 2)
+            const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
             for (int d = 0; d < nd; ++d) {
-                Acc* dst = dsts[d];
+                Acc* dst = p.fused_mode == 2
+                               ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
+                               : static_cast<Acc*>(p.out_recs) + g * REC;
 #pragma unroll
                 for (int sw = 0; sw < kSweeps; ++sw) {
                     const int j = sw * kPer + lane * kVW;
