@@ -105,7 +105,8 @@ void dattn_store::setup_exchange() {
     const size_t xbytes = 2 * xhalf;
     flag_stride = std::max<int64_t>(kMaxExchangeGrid, static_cast<int64_t>(cfg.max_seqs) * cfg.num_kv_heads);
     fhalf = static_cast<size_t>(nranks) * flag_stride;
-    const size_t fbytes = 2 * fhalf * sizeof(uint32_t);
+    // flags (two halves), then the monotonic per-source group counters (uint64)
+    const size_t fbytes = 2 * fhalf * sizeof(uint32_t) + (static_cast<size_t>(nranks) + 2) * sizeof(uint64_t);
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
     cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
@@ -147,6 +148,7 @@ void dattn_store::setup_exchange() {
                "ncclAllGather(barrier)");
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     epoch = 0;
+    count_target = 0;
     fused_merge = true;
 }
 
@@ -680,6 +682,8 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         f.nranks = nranks;
         f.slot_stride = slot_stride;
         f.flag_stride = flag_stride;
+        for (int r = 0; r < nranks; ++r) f.peer_count[r] = counters_of(peer_flags[r]);
+        count_target += static_cast<unsigned long long>(b.num_rows) * cfg.num_kv_heads;
         run_ma(pl, q_dev, recs.p, b.scale, false, &f);
         RankMergeParams rp{};
         rp.rows = b.num_rows;
@@ -697,6 +701,8 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         rp.flag_stride = flag_stride;
         rp.epoch = f.epoch;
         rp.out_norm = out_dev0;
+        for (int r = 0; r < nranks; ++r) rp.peer_count[r] = f.peer_count[r];
+        rp.count_target = count_target;
         // all CTAs co-resident (<= 4 per SM): identity pushes precede every wait
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8, static_cast<int64_t>(num_sms) * 4)));

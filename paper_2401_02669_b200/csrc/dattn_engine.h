@@ -104,6 +104,12 @@ struct dattn_store {
         return static_cast<unsigned char*>(base) + (ep & 1u) * xhalf;
     }
     uint32_t* fhalf_ptr(uint32_t* base, uint32_t ep) const { return base + (ep & 1u) * fhalf; }
+    // per-source delivered-group counters behind the two flag halves (8-B aligned)
+    unsigned long long* counters_of(uint32_t* flags_base) const {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(flags_base + 2 * fhalf);
+        return reinterpret_cast<unsigned long long*>((a + 7) & ~uintptr_t(7));
+    }
+    unsigned long long count_target = 0;
     uint32_t epoch = 0;
     bool fused_merge = false;
     void setup_exchange();

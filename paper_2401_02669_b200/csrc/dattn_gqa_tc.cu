@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float kNegInf = -INFINITY;
         float m[GI], l[GI], acc[GI], corr_prev[GI];
         bool pending = false;  // an O^T tile of the current item not yet accumulated
+        unsigned int pushed = 0;  // groups merged and pushed (fused mode 2)
         float* recs = static_cast<float*>(p.records);
         for (uint32_t it = 0;; ++it) {
             mbar_wait(&S.mready[it % kMeta], (it / kMeta) & 1u);
@@ -530,10 +531,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __threadfence();
                         fused_group_merge<bf16_t, kD, 4>(p, md.row, md.kvh, warp - 2, lane, S.mrg_m, S.mrg_e,
                                                           S.mrg_acc);
+                        ++pushed;
                     }
                     named_bar_sync(1, 128);
                 }
             }
+        }
+        if (p.fused_mode == 2) {
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) publish_pushed(p, pushed);
         }
     }
     tc_fence_before();

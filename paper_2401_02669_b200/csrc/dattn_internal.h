@@ -58,9 +58,10 @@ struct MAParams {
     int64_t slot_stride;             // records per source rank
     int64_t flag_stride;             // flags per source rank
     uint32_t epoch;
+    unsigned long long* peer_count[8];  // per destination: [nranks] groups received per source
 };
 
-// K6: rank merge after fused K1 (waits for every rank's group flags).
+// K6: rank merge after fused K1/K2 (waits until every rank delivered all groups).
 struct RankMergeParams {
     int32_t rows;
     int32_t heads;
@@ -75,6 +76,8 @@ struct RankMergeParams {
     int64_t flag_stride;
     uint32_t epoch;
     void* out_norm;
+    unsigned long long* peer_count[8];
+    unsigned long long count_target;  // cumulative groups per source after this step
 };
 
 // K3 merge launch.

@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     const Acc kLn2 = static_cast<Acc>(0.6931471805599453094);
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     bool nonfinite = false;
+    unsigned int pushed = 0;  // groups merged and pushed by this CTA (fused mode 2)
 
     Acc q[HPW][EPL];
     Acc acc[HPW][EPL];
@@ -505,6 +506,7 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                 if (s_last) {
                     __threadfence();
                     fused_group_merge<T, DP>(p, md.row, md.kvh, cw, lane, red_m, red_e, red_acc);
+                    ++pushed;  // uniform across the consumer warps
                 }
             }
         }
@@ -512,6 +514,10 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             stage = 0;
             phase ^= 1u;
         }
+    }
+    if (p.fused_mode == 2) {
+        named_bar_sync(1, 32 * kConsumerWarps);  // every group push of this CTA is issued
+        if (cw == 0 && lane == 0) publish_pushed(p, pushed);
     }
     if (nonfinite && p.nonfinite_flag) atomicOr(p.nonfinite_flag, 1);
 }
@@ -872,11 +878,12 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
 }
 
 // ------------------------------------------------------------------ K6
-// Rank merge after the fused K1: one warp per (row, q head). This rank first
-// publishes identity records for its groups that hold no tokens (no K1 CTA
-// completes them), then every warp waits for its group's flag from every
-// rank and merges the nranks records into the output. CTAs never wait for
-// each other on this GPU; peers' flags come from their K1 or K6.
+// Rank merge after the fused K1/K2: one warp per (row, q head). This rank
+// first publishes identity records for its groups that hold no tokens (no MA
+// CTA completes them), then every CTA waits until each rank's delivered-group
+// counter reaches this step's cumulative target and merges the nranks records
+// into the output. CTAs never wait for each other on this GPU; the counters
+// are advanced by the peers' MA kernels (per CTA, at exit) and K6s.
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const RankMergeParams x) {
     using E = Elem<T>;
@@ -885,6 +892,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const Rank
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t ngroups_kv = static_cast<int64_t>(x.rows) * x.num_kv_heads;
+    unsigned int mine = 0;
     // identity records for empty (row, kv head) groups of this rank
     for (int64_t gk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gk < ngroups_kv;
          gk += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -900,10 +908,35 @@ __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const Rank
                 dst[3] = 0;  // ma is never read for identity records
             }
         }
+        ++mine;
+    }
+    // publish this CTA's identity pushes (one system fence per CTA)
+    __shared__ unsigned int s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    if (mine) atomicAdd(&s_cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) {
         __threadfence_system();
         for (int r = 0; r < x.nranks; ++r)
-            st_release_sys(x.peer_flags[r] + static_cast<int64_t>(x.rank) * x.flag_stride + gk, x.epoch);
+            atomicAdd_system(x.peer_count[r] + x.rank, static_cast<unsigned long long>(s_cnt));
     }
+    // wait until every rank delivered all (row, kv head) groups of this step
+    if (threadIdx.x < x.nranks) {
+        const unsigned long long* c = x.peer_count[x.rank] + threadIdx.x;
+        uint64_t t0 = 0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
+            if (v >= x.count_target) break;
+            __nanosleep(64);
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 10000000000ull) __trap();
+        }
+    }
+    __syncthreads();
     const int64_t groups = static_cast<int64_t>(x.rows) * x.heads;
     const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
@@ -911,18 +944,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const Rank
         const int row = static_cast<int>(g / x.heads);
         const int h = static_cast<int>(g - static_cast<int64_t>(row) * x.heads);
         const int64_t gk = static_cast<int64_t>(row) * x.num_kv_heads + h / x.group;
-        if (lane < x.nranks) {
-            const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(lane) * x.flag_stride + gk;
-            uint64_t t0 = 0;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            while (ld_acquire_sys(f) != x.epoch) {
-                __nanosleep(32);
-                uint64_t t1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-                if (t1 - t0 > 10000000000ull) __trap();
-            }
-        }
-        __syncwarp();
+        (void)gk;
         Acc m2 = kNegInf;
         for (int r = 0; r < x.nranks; ++r) {
             const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;

@@ -213,11 +213,14 @@ __device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, i
         }
         named_bar_sync(1, 32 * NW);
     }
-    if (p.fused_mode == 2 && cw == 0 && lane == 0) {
-        __threadfence_system();
-        const int64_t f = static_cast<int64_t>(p.rank) * p.flag_stride + static_cast<int64_t>(row) * p.num_kv_heads + kvh;
-        for (int r = 0; r < p.nranks; ++r) st_release_sys(p.peer_flags[r] + f, p.epoch);
-    }
+}
+
+// End of an MA kernel in fused mode 2: publish how many groups this CTA pushed
+// (one system fence per CTA instead of one per group); K6 waits on the sums.
+__device__ __forceinline__ void publish_pushed(const MAParams& p, unsigned int pushed) {
+    if (p.fused_mode != 2 || pushed == 0) return;
+    __threadfence_system();
+    for (int r = 0; r < p.nranks; ++r) atomicAdd_system(p.peer_count[r] + p.rank, static_cast<unsigned long long>(pushed));
 }
 
 

@@ -257,7 +257,8 @@ def test_fused_group_merge_equals_separate_merge(torch_cuda, hq, hkv):
         sep = out_np(torch, decode(torch, st, rg, 7, q), 128)
     finally:
         del os.environ["DATTN_FUSED_K1"]
-    assert rel_errs(fused[:6], sep[:6]) < 1e-5
+    # bf16 outputs: fp32 re-association may flip the last bf16 bit
+    assert rel_errs(fused[:6], sep[:6]) < 4e-3
     assert not fused[6].any() and not sep[6].any()  # row without ranges
     # repeated launches reuse the self-resetting completion counters
     again = out_np(torch, decode(torch, st, rg, 7, q), 128)
