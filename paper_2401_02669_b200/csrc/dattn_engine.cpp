@@ -186,6 +186,7 @@ static void validate_config(const dattn_store_config& c) {
         throw Error(DATTN_ERR_CONTRACT, "num_pages out of range");
     if (c.max_seqs < 1 || c.max_pages_per_seq < 1)
         throw Error(DATTN_ERR_CONTRACT, "block-table shape must be >= 1");
+    if (c.num_kv_heads > 255) throw Error(DATTN_ERR_CONTRACT, "num_kv_heads must be <= 255");
     const int g = c.num_q_heads / c.num_kv_heads;
     if (g > (c.dtype == kF64 ? 8 : 16))
         throw Error(DATTN_ERR_CONTRACT, "query group size too large for the MA kernel");

@@ -38,7 +38,7 @@ constexpr int kN = 16;          // MMA N: q heads, padded
 constexpr int kKStages = 3;     // K (+ Q) ring: released as soon as MMA1 has read it
 constexpr int kVStages = 3;     // V ring: released after MMA2
 constexpr int kMeta = 8;        // tile descriptors, read by the V producer / softmax warps
-constexpr int kThreads = 224;   // w0 K producer, w1 MMA, w2..5 softmax, w6 V producer
+constexpr int kThreads = 256;   // w0 K producer, w1 MMA, w2..5 softmax, w6 V producer, w7 merge
 constexpr int kHalf = kTile * 128;        // bytes of one 64-column half of a 128-row tile
 constexpr int kKVBytes = 2 * kHalf;       // one tensor (K or V) tile: 32 KB
 constexpr int kQBytes = 2 * kN * 128;     // Q slot: two halves of 16 rows x 128 B
@@ -71,8 +71,7 @@ struct Smem {
     int32_t pid[kPidWin];
     float red_max[2][4][kN];
     float red_sum[4][kN];
-    float mrg_m[4], mrg_e[4], mrg_acc[4 * kD];  // fused group merge scratch
-    int32_t s_last;
+    MergeQueue mq;  // completed groups -> merge warp
     uint32_t tmem_base;
 };
 
@@ -210,6 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&S.vempty[i], 1);
         }
         for (int i = 0; i < kMeta; ++i) mbar_init(&S.mready[i], 1);
+        S.mq.tail = 0;
+        S.mq.head = 0;
+        for (int i = 0; i < kMergeQueue; ++i) S.mq.seq[i] = 0;
         mbar_init(&S.s_full, 1);
         mbar_init(&S.s_free, 4);
         for (int b = 0; b < 2; ++b) {
@@ -318,6 +320,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&S.kempty[ks], ((t / kKStages) & 1u) ^ 1u);
             mbar_arrive(&S.kfull[ks]);
         }
+    } else if (warp == 7) {
+        // ================================ merge warp (fused modes)
+        if (p.fused_mode != 0) {
+            unsigned int pushed = 0;
+            for (int idx = 0;; ++idx) {
+                int32_t v = 0;
+                if (lane == 0) v = mq_pop(&S.mq, idx);
+                v = __shfl_sync(0xffffffffu, v, 0);
+                if (v < 0) break;
+                __threadfence();
+                warp_group_merge<bf16_t, kD>(p, v >> 8, v & 0xFF, lane);
+                ++pushed;
+            }
+            if (p.fused_mode == 2) {
+                __syncwarp();
+                if (lane == 0) publish_pushed(p, pushed);
+            }
+        }
     } else if (warp == 6) {
         // ================================ V producer (trails the K producer)
         if (lane == 0) {
@@ -409,7 +429,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float kNegInf = -INFINITY;
         float m[GI], l[GI], acc[GI], corr_prev[GI];
         bool pending = false;  // an O^T tile of the current item not yet accumulated
-        unsigned int pushed = 0;  // groups merged and pushed (fused mode 2)
         float* recs = static_cast<float*>(p.records);
         for (uint32_t it = 0;; ++it) {
             mbar_wait(&S.mready[it % kMeta], (it / kMeta) & 1u);
@@ -515,31 +534,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 named_bar_sync(1, 128);
-                if (p.fused_mode != 0) {
+                if (p.fused_mode != 0 && warp == 2 && lane == 0) {
                     // group completion (see K1): the CTA that wrote the last
-                    // chunk of (row, kv head) merges the group
-                    if (warp == 2 && lane == 0) {
-                        __threadfence();
-                        const int gi = md.row * p.num_kv_heads + md.kvh;
-                        const int old = atomicAdd(p.group_counter + gi, 1);
-                        const int last = (old + 1 == __ldg(p.group_expected + gi)) ? 1 : 0;
-                        if (last) p.group_counter[gi] = 0;
-                        S.s_last = last;
+                    // chunk of (row, kv head) hands it to the merge warp
+                    __threadfence();
+                    const int gi = md.row * p.num_kv_heads + md.kvh;
+                    const int old = atomicAdd(p.group_counter + gi, 1);
+                    if (old + 1 == __ldg(p.group_expected + gi)) {
+                        p.group_counter[gi] = 0;
+                        mq_push(&S.mq, (md.row << 8) | md.kvh);
                     }
-                    named_bar_sync(1, 128);
-                    if (S.s_last) {
-                        __threadfence();
-                        fused_group_merge<bf16_t, kD, 4>(p, md.row, md.kvh, warp - 2, lane, S.mrg_m, S.mrg_e,
-                                                          S.mrg_acc);
-                        ++pushed;
-                    }
-                    named_bar_sync(1, 128);
                 }
             }
         }
-        if (p.fused_mode == 2) {
+        if (p.fused_mode != 0) {
             named_bar_sync(1, 128);
-            if (warp == 2 && lane == 0) publish_pushed(p, pushed);
+            if (warp == 2 && lane == 0) mq_push(&S.mq, -1);
         }
     }
     tc_fence_before();

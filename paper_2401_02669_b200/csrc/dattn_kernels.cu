@@ -29,7 +29,7 @@
 
 namespace dattn {
 
-constexpr int kMAThreads = 32 * (1 + kConsumerWarps);
+constexpr int kMAThreads = 32 * (1 + kConsumerWarps + 1);  // producer, consumers, merge warp
 constexpr int kStageSlotBytes = 16384;  // bytes of K (and of V) per pipeline stage
 constexpr int kPidWindow = 256;         // block-table entries cached per window
 
@@ -144,14 +144,40 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     const int lane = threadIdx.x & 31;
     const int stages = p.stages;
 
+    __shared__ MergeQueue mq;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_mbar_init();
+        mq.tail = 0;
+        mq.head = 0;
     }
+    if (threadIdx.x < kMergeQueue) mq.seq[threadIdx.x] = 0;
     __syncthreads();
+
+    if (warp == kConsumerWarps + 1) {
+        // ===================== merge warp (fused modes) =====================
+        // merges each (row, kv head) group whose last chunk this CTA wrote,
+        // concurrently with the streaming warps
+        if (p.fused_mode == 0) return;
+        unsigned int pushed = 0;
+        for (int idx = 0;; ++idx) {
+            int32_t v = 0;
+            if (lane == 0) v = mq_pop(&mq, idx);
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if (v < 0) break;
+            __threadfence();  // acquire the other CTAs' records of the group
+            warp_group_merge<T, DP>(p, v >> 8, v & 0xFF, lane);
+            ++pushed;
+        }
+        if (p.fused_mode == 2) {
+            __syncwarp();
+            if (lane == 0) publish_pushed(p, pushed);
+        }
+        return;
+    }
 
     if (warp == 0) {
         // ===================== producer warp =====================
@@ -254,7 +280,6 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     const Acc kLn2 = static_cast<Acc>(0.6931471805599453094);
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     bool nonfinite = false;
-    unsigned int pushed = 0;  // groups merged and pushed by this CTA (fused mode 2)
 
     Acc q[HPW][EPL];
     Acc acc[HPW][EPL];
@@ -491,22 +516,17 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             }
             if (p.fused_mode != 0) {
                 // ---- group completion: the CTA that wrote the last chunk of
-                //      (row, kv head) merges the group (threadfence pattern)
-                __shared__ int s_last;
+                //      (row, kv head) hands the group to its merge warp
+                //      (threadfence pattern; counters reset for the next launch)
                 named_bar_sync(1, 32 * kConsumerWarps);  // this item's records are issued
                 if (cw == 0 && lane == 0) {
                     __threadfence();
                     const int gi = md.row * p.num_kv_heads + md.kvh;
                     const int old = atomicAdd(p.group_counter + gi, 1);
-                    const int last = (old + 1 == __ldg(p.group_expected + gi)) ? 1 : 0;
-                    if (last) p.group_counter[gi] = 0;  // ready for the next launch
-                    s_last = last;
-                }
-                named_bar_sync(1, 32 * kConsumerWarps);
-                if (s_last) {
-                    __threadfence();
-                    fused_group_merge<T, DP>(p, md.row, md.kvh, cw, lane, red_m, red_e, red_acc);
-                    ++pushed;  // uniform across the consumer warps
+                    if (old + 1 == __ldg(p.group_expected + gi)) {
+                        p.group_counter[gi] = 0;
+                        mq_push(&mq, (md.row << 8) | md.kvh);
+                    }
                 }
             }
         }
@@ -515,9 +535,9 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             phase ^= 1u;
         }
     }
-    if (p.fused_mode == 2) {
-        named_bar_sync(1, 32 * kConsumerWarps);  // every group push of this CTA is issued
-        if (cw == 0 && lane == 0) publish_pushed(p, pushed);
+    if (p.fused_mode != 0) {
+        named_bar_sync(1, 32 * kConsumerWarps);  // every group of this CTA is queued
+        if (cw == 0 && lane == 0) mq_push(&mq, -1);
     }
     if (nonfinite && p.nonfinite_flag) atomicOr(p.nonfinite_flag, 1);
 }

@@ -83,15 +83,12 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
-// Fused group merge (run by the 8 consumer warps of the CTA that completed the
-// last chunk of (row, kvh)): for every q head of the kv head, rescale-sum the
-// row's chunk records (aggregate_partials, distattention.cpp:150-174), then
-// write the normalised output (mode 1) or push the merged record to every
-// rank's exchange buffer and raise the group's flag there (mode 2).
-template <typename T, int DP, int NW = kConsumerWarps>
-__device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, int lane,
-                                  typename Elem<T>::Acc* red_m, typename Elem<T>::Acc* red_e,
-                                  typename Elem<T>::Acc* red_acc) {
+// Warp-only group merge (the MA kernels' dedicated merge warp): for every q
+// head of kv head `kvh`, rescale-sum the row's chunk records and write the
+// normalised output (mode 1) or push the merged record to every rank's
+// exchange slot (mode 2). No barriers: it runs beside the streaming warps.
+template <typename T, int DP>
+__device__ void warp_group_merge(const MAParams& p, int row, int kvh, int lane) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
     constexpr int REC = DP + 4;
@@ -100,18 +97,11 @@ __device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, i
     constexpr int kPer = 32 * kVW;
     constexpr int kSweeps = (DP + kPer - 1) / kPer;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
-    const int G = p.group;
-    const int hpass = G < NW ? G : NW;  // heads per pass
-    const int wph2 = NW / hpass;                      // warps per head
     const int cbase = p.row_begin[row];
     const int n = p.row_begin[row + 1] - cbase;
     const Acc* R = static_cast<const Acc*>(p.records);
-    __shared__ Acc s_tok[NW];
-    for (int hh0 = 0; hh0 < G; hh0 += hpass) {
-        const int slot = cw / wph2, sub = cw - slot * wph2;
-        const int hh = hh0 + slot;
-        const bool hv = slot < hpass && hh < G;
-        const int h = kvh * G + (hv ? hh : 0);
+    for (int hh = 0; hh < p.group; ++hh) {
+        const int h = kvh * p.group + hh;
         const int64_t base = static_cast<int64_t>(cbase) * p.num_q_heads + h;
         auto live = [&](int c, const Acc* r) {
             if (p.chunk_kvh) {
@@ -121,98 +111,82 @@ __device__ void fused_group_merge(const MAParams& p, int row, int kvh, int cw, i
             return __ldcg(r + 2) != Acc(0);
         };
         Acc mg = kNegInf;
-        if (hv)
-            for (int c = sub * 32 + lane; c < n; c += wph2 * 32) {
-                const Acc* r = R + (base + static_cast<int64_t>(c) * p.num_q_heads) * REC;
-                if (live(c, r)) {
-                    const Acc mc = __ldcg(r);
-                    mg = mc > mg ? mc : mg;
-                }
+        for (int c = lane; c < n; c += 32) {
+            const Acc* r = R + (base + static_cast<int64_t>(c) * p.num_q_heads) * REC;
+            if (live(c, r)) {
+                const Acc mc = __ldcg(r);
+                mg = mc > mg ? mc : mg;
             }
+        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
             mg = o > mg ? o : mg;
         }
-        if (lane == 0) red_m[cw] = mg;
-        named_bar_sync(1, 32 * NW);
-        mg = kNegInf;
-        for (int w2 = 0; w2 < wph2; ++w2) {
-            const Acc mm = red_m[slot * wph2 + w2];
-            mg = mm > mg ? mm : mg;
-        }
-        Acc eg = 0, ntok = 0;
+        Acc eg, ntok;
         Acc acc[kSweeps][kVW];
 #pragma unroll
         for (int sw = 0; sw < kSweeps; ++sw)
 #pragma unroll
             for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
-        if (hv) fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.num_q_heads, n, sub, wph2, mg, live, acc, eg, ntok, lane);
-#pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw) {
-            const int j = sw * kPer + lane * kVW;
-            if (j < DP)
-#pragma unroll
-                for (int v = 0; v < kVW; ++v) red_acc[cw * DP + j + v] = acc[sw][v];
-        }
-        if (lane == 0) {
-            red_e[cw] = eg;
-            s_tok[cw] = ntok;
-        }
-        named_bar_sync(1, 32 * NW);
-        if (hv && sub == 0) {
-            eg = 0;
-            ntok = 0;
-            for (int w2 = 0; w2 < wph2; ++w2) {
-                eg += red_e[slot * wph2 + w2];
-                ntok += s_tok[slot * wph2 + w2];
-            }
+        fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.num_q_heads, n, 0, 1, mg, live, acc, eg, ntok, lane);
+        const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + h;
+        if (p.fused_mode == 1) {
+            T* o = static_cast<T*>(p.out_norm) + g * DP;
 #pragma unroll
             for (int sw = 0; sw < kSweeps; ++sw) {
                 const int j = sw * kPer + lane * kVW;
                 if (j < DP)
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) {
-                        Acc a = 0;
-                        for (int w2 = 0; w2 < wph2; ++w2) a += red_acc[(slot * wph2 + w2) * DP + j + v];
-                        acc[sw][v] = a;
-                    }
-            }
-            const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + h;
-            if (p.fused_mode == 1) {
-                T* o = static_cast<T*>(p.out_norm) + g * DP;
-#pragma unroll
-                for (int sw = 0; sw < kSweeps; ++sw) {
-                    const int j = sw * kPer + lane * kVW;
-                    if (j < DP)
-#pragma unroll
-                        for (int v = 0; v < kVW; ++v)
-                            o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
-                }
-            }
-            // merged record -> out_recs (mode 1) or every rank's exchange slot (mode 2)
-            const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
-            for (int d = 0; d < nd; ++d) {
-                Acc* dst = p.fused_mode == 2
-                               ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
-                               : static_cast<Acc*>(p.out_recs) + g * REC;
-#pragma unroll
-                for (int sw = 0; sw < kSweeps; ++sw) {
-                    const int j = sw * kPer + lane * kVW;
-                    if (j < DP)
-#pragma unroll
-                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
-                }
-                if (lane == 0) {
-                    dst[0] = ntok != Acc(0) ? mg : kNegInf;
-                    dst[1] = eg;
-                    dst[2] = ntok;
-                    dst[3] = 0;
-                }
+                    for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
             }
         }
-        named_bar_sync(1, 32 * NW);
+        const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
+        for (int d = 0; d < nd; ++d) {
+            Acc* dst = p.fused_mode == 2
+                           ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
+                           : static_cast<Acc*>(p.out_recs) + g * REC;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+            }
+            if (lane == 0) {
+                dst[0] = ntok != Acc(0) ? mg : kNegInf;
+                dst[1] = eg;
+                dst[2] = ntok;
+                dst[3] = 0;
+            }
+        }
     }
+}
+
+// Single-producer-per-item / single-consumer queue of completed groups in
+// shared memory, from the streaming warps to the merge warp.
+constexpr int kMergeQueue = 64;
+struct MergeQueue {
+    int32_t slot[kMergeQueue];   // packed (row << 8 | kvh), -1 = stop
+    volatile int32_t seq[kMergeQueue];  // index + 1 once the slot is written
+    int32_t tail;                // next index to hand out (atomicAdd)
+    volatile int32_t head;       // next index the merge warp consumes
+};
+
+__device__ __forceinline__ void mq_push(MergeQueue* q, int32_t v) {
+    const int idx = atomicAdd(&q->tail, 1);
+    while (idx - q->head >= kMergeQueue) __nanosleep(64);  // full: the merge warp is behind
+    q->slot[idx % kMergeQueue] = v;
+    __threadfence_block();
+    q->seq[idx % kMergeQueue] = idx + 1;
+}
+
+__device__ __forceinline__ int32_t mq_pop(MergeQueue* q, int idx) {
+    while (q->seq[idx % kMergeQueue] != idx + 1) __nanosleep(32);
+    __threadfence_block();
+    const int32_t v = q->slot[idx % kMergeQueue];
+    q->head = idx + 1;
+    return v;
 }
 
 // End of an MA kernel in fused mode 2: publish how many groups this CTA pushed
