@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v = __shfl_sync(0xffffffffu, v, 0);
                 if (v < 0) break;
                 __threadfence();
-                warp_group_merge<bf16_t, kD>(p, v >> 8, v & 0xFF, lane);
+                warp_group_merge<bf16_t, kD, (GI < 8 ? GI : 8)>(p, v >> 8, v & 0xFF, lane);
                 ++pushed;
             }
             if (p.fused_mode == 2) {

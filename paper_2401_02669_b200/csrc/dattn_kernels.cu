@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             v = __shfl_sync(0xffffffffu, v, 0);
             if (v < 0) break;
             __threadfence();  // acquire the other CTAs' records of the group
-            warp_group_merge<T, DP>(p, v >> 8, v & 0xFF, lane);
+            warp_group_merge<T, DP, (sizeof(T) == 8 ? 2 : 8)>(p, v >> 8, v & 0xFF, lane);
             ++pushed;
         }
         if (p.fused_mode == 2) {

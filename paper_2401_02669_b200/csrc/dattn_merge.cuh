@@ -87,7 +87,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 // head of kv head `kvh`, rescale-sum the row's chunk records and write the
 // normalised output (mode 1) or push the merged record to every rank's
 // exchange slot (mode 2). No barriers: it runs beside the streaming warps.
-template <typename T, int DP>
+// Up to MAXG heads are folded together so each chunk step issues MAXG
+// independent loads (the heads of a chunk are adjacent records).
+template <typename T, int DP, int MAXG>
 __device__ void warp_group_merge(const MAParams& p, int row, int kvh, int lane) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
@@ -100,64 +102,130 @@ __device__ void warp_group_merge(const MAParams& p, int row, int kvh, int lane) 
     const int cbase = p.row_begin[row];
     const int n = p.row_begin[row + 1] - cbase;
     const Acc* R = static_cast<const Acc*>(p.records);
-    for (int hh = 0; hh < p.group; ++hh) {
-        const int h = kvh * p.group + hh;
-        const int64_t base = static_cast<int64_t>(cbase) * p.num_q_heads + h;
-        auto live = [&](int c, const Acc* r) {
-            if (p.chunk_kvh) {
-                const int tag = p.chunk_kvh[cbase + c];
-                if (tag >= 0 && tag != kvh) return false;
-            }
-            return __ldcg(r + 2) != Acc(0);
+    for (int h0 = 0; h0 < p.group; h0 += MAXG) {
+        const int nh = min(MAXG, p.group - h0);
+        const int64_t base = static_cast<int64_t>(cbase) * p.num_q_heads + static_cast<int64_t>(kvh) * p.group + h0;
+        auto rec_of = [&](int c, int hh) { return R + (base + static_cast<int64_t>(c) * p.num_q_heads + hh) * REC; };
+        auto chunk_live = [&](int c) {
+            if (!p.chunk_kvh) return true;
+            const int tag = p.chunk_kvh[cbase + c];
+            return tag < 0 || tag == kvh;
         };
-        Acc mg = kNegInf;
+        // pass 1: per-head max over live records (lanes over chunks)
+        Acc mg[MAXG];
+#pragma unroll
+        for (int hh = 0; hh < MAXG; ++hh) mg[hh] = kNegInf;
         for (int c = lane; c < n; c += 32) {
-            const Acc* r = R + (base + static_cast<int64_t>(c) * p.num_q_heads) * REC;
-            if (live(c, r)) {
-                const Acc mc = __ldcg(r);
-                mg = mc > mg ? mc : mg;
+            if (!chunk_live(c)) continue;
+#pragma unroll
+            for (int hh = 0; hh < MAXG; ++hh) {
+                if (hh >= nh) continue;
+                const Acc* r = rec_of(c, hh);
+                const Acc tk = __ldcg(r + 2), mc = __ldcg(r);
+                if (tk != Acc(0)) mg[hh] = mc > mg[hh] ? mc : mg[hh];
             }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
-            mg = o > mg ? o : mg;
+        for (int hh = 0; hh < MAXG; ++hh)
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const Acc o = __shfl_xor_sync(0xffffffffu, mg[hh], off);
+                mg[hh] = o > mg[hh] ? o : mg[hh];
+            }
+        // pass 2: rounds of 32 chunks: lane weights, then a broadcast fold
+        Acc e_l[MAXG], t_l[MAXG];
+        Acc acc[MAXG][kSweeps][kVW];
+#pragma unroll
+        for (int hh = 0; hh < MAXG; ++hh) {
+            e_l[hh] = t_l[hh] = 0;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) acc[hh][sw][v] = 0;
         }
-        Acc eg, ntok;
-        Acc acc[kSweeps][kVW];
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int c = i0 + lane;
+            Acc w[MAXG];
+            const bool cl = c < n && chunk_live(c);
 #pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw)
+            for (int hh = 0; hh < MAXG; ++hh) {
+                w[hh] = 0;
+                if (cl && hh < nh) {
+                    const Acc* r = rec_of(c, hh);
+                    const Acc tk = __ldcg(r + 2);
+                    if (tk != Acc(0)) {
+                        const Acc mc = __ldcg(r);
+                        w[hh] = (mc == mg[hh]) ? Acc(1) : exp(mc - mg[hh]);
+                        e_l[hh] += __ldcg(r + 1) * w[hh];
+                        t_l[hh] += tk;
+                    }
+                }
+            }
+            const int cnt = min(32, n - i0);
+            for (int k = 0; k < cnt; ++k) {
 #pragma unroll
-            for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
-        fold_chunks<Acc, DP, kVW, kSweeps>(R, base, p.num_q_heads, n, 0, 1, mg, live, acc, eg, ntok, lane);
-        const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + h;
-        if (p.fused_mode == 1) {
-            T* o = static_cast<T*>(p.out_norm) + g * DP;
+                for (int hh = 0; hh < MAXG; ++hh) {
+                    if (hh >= nh) continue;
+                    const Acc wk = __shfl_sync(0xffffffffu, w[hh], k);
+                    const Acc* r = rec_of(i0 + k, hh);
 #pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP)
+                    for (int sw = 0; sw < kSweeps; ++sw) {
+                        const int j = sw * kPer + lane * kVW;
+                        if (j < DP) {
+                            if constexpr (kVW == 4) {
+                                const float4 x = __ldcg(reinterpret_cast<const float4*>(r + 4 + j));
+                                acc[hh][sw][0] += x.x * wk; acc[hh][sw][1] += x.y * wk;
+                                acc[hh][sw][2] += x.z * wk; acc[hh][sw][3] += x.w * wk;
+                            } else {
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(ntok != Acc(0) ? acc[sw][v] / eg : Acc(0));
+                                for (int v = 0; v < kVW; ++v) acc[hh][sw][v] += __ldcg(r + 4 + j + v) * wk;
+                            }
+                        }
+                    }
+                }
             }
         }
-        const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
-        for (int d = 0; d < nd; ++d) {
-            Acc* dst = p.fused_mode == 2
-                           ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
-                           : static_cast<Acc*>(p.out_recs) + g * REC;
 #pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP)
+        for (int hh = 0; hh < MAXG; ++hh)
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+            for (int off = 16; off > 0; off >>= 1) {
+                e_l[hh] += __shfl_xor_sync(0xffffffffu, e_l[hh], off);
+                t_l[hh] += __shfl_xor_sync(0xffffffffu, t_l[hh], off);
             }
-            if (lane == 0) {
-                dst[0] = ntok != Acc(0) ? mg : kNegInf;
-                dst[1] = eg;
-                dst[2] = ntok;
-                dst[3] = 0;
+#pragma unroll
+        for (int hh = 0; hh < MAXG; ++hh) {
+            if (hh >= nh) continue;
+            const Acc eg = e_l[hh], ntok = t_l[hh];
+            const int64_t g = static_cast<int64_t>(row) * p.num_q_heads + static_cast<int64_t>(kvh) * p.group + h0 + hh;
+            if (p.fused_mode == 1) {
+                T* o = static_cast<T*>(p.out_norm) + g * DP;
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v)
+                            o[j + v] = E::from_acc(ntok != Acc(0) ? acc[hh][sw][v] / eg : Acc(0));
+                }
+            }
+            const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
+            for (int d = 0; d < nd; ++d) {
+                Acc* dst = p.fused_mode == 2
+                               ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
+                               : static_cast<Acc*>(p.out_recs) + g * REC;
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP)
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[hh][sw][v];
+                }
+                if (lane == 0) {
+                    dst[0] = ntok != Acc(0) ? mg[hh] : kNegInf;
+                    dst[1] = eg;
+                    dst[2] = ntok;
+                    dst[3] = 0;
+                }
             }
         }
     }
