@@ -537,9 +537,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.fused_mode != 0 && warp == 2 && lane == 0) {
                     // group completion (see K1): the CTA that wrote the last
                     // chunk of (row, kv head) hands it to the merge warp
-                    __threadfence();
                     const int gi = md.row * p.num_kv_heads + md.kvh;
-                    const int old = atomicAdd(p.group_counter + gi, 1);
+                    const int old = atomic_add_acq_rel_gpu(p.group_counter + gi, 1);
                     if (old + 1 == __ldg(p.group_expected + gi)) {
                         p.group_counter[gi] = 0;
                         mq_push(&S.mq, (md.row << 8) | md.kvh);

@@ -520,9 +520,8 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
                 //      (threadfence pattern; counters reset for the next launch)
                 named_bar_sync(1, 32 * kConsumerWarps);  // this item's records are issued
                 if (cw == 0 && lane == 0) {
-                    __threadfence();
                     const int gi = md.row * p.num_kv_heads + md.kvh;
-                    const int old = atomicAdd(p.group_counter + gi, 1);
+                    const int old = atomic_add_acq_rel_gpu(p.group_counter + gi, 1);
                     if (old + 1 == __ldg(p.group_expected + gi)) {
                         p.group_counter[gi] = 0;
                         mq_push(&mq, (md.row << 8) | md.kvh);

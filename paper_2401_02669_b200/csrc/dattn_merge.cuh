@@ -241,6 +241,16 @@ struct MergeQueue {
     volatile int32_t head;       // next index the merge warp consumes
 };
 
+// Completion-count increment with acq_rel semantics at gpu scope: after a CTA
+// barrier, one thread's release is cumulative over the CTA's record stores
+// (the pattern CUTLASS semaphores use), and the acquire side sees every other
+// CTA's records of the group -- no full __threadfence on the streaming path.
+__device__ __forceinline__ int atomic_add_acq_rel_gpu(int32_t* p, int32_t v) {
+    int32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void mq_push(MergeQueue* q, int32_t v) {
     const int idx = atomicAdd(&q->tail, 1);
     while (idx - q->head >= kMergeQueue) __nanosleep(64);  // full: the merge warp is behind
@@ -250,7 +260,7 @@ __device__ __forceinline__ void mq_push(MergeQueue* q, int32_t v) {
 }
 
 __device__ __forceinline__ int32_t mq_pop(MergeQueue* q, int idx) {
-    while (q->seq[idx % kMergeQueue] != idx + 1) __nanosleep(32);
+    while (q->seq[idx % kMergeQueue] != idx + 1) __nanosleep(200);  // gentle: not on the critical path
     __threadfence_block();
     const int32_t v = q->slot[idx % kMergeQueue];
     q->head = idx + 1;
