@@ -423,14 +423,16 @@ void dattn_store::upload_plan(const Plan& pl) {
     meta_valid = true;
 }
 
-// The fused group merge needs the K1 kernel (K2 keeps the separate merges)
-// and is switched off by DATTN_FUSED_K1=0.
+// In-kernel group merge (merge warp + completion counters; §5.4 of DESIGN.md)
+// is opt-in with DATTN_FUSED_K1=1: measured on B200 it loses to the separate
+// merge launches (K3 on one GPU, K5 across GPUs) because heavy groups finish
+// at the very end of the MA kernel and their merge becomes its tail. The
+// decision depends only on the environment, so every rank agrees.
 bool dattn_store::fused_ok(const Plan& pl, bool check_finite) const {
-    const char* env = std::getenv("DATTN_FUSED_K1");
-    if (env && std::atoi(env) == 0) return false;
-    (void)pl;  // rank-independent on purpose: every rank of a sharded step must agree
+    (void)pl;
     (void)check_finite;
-    return true;
+    const char* env = std::getenv("DATTN_FUSED_K1");
+    return env && std::atoi(env) == 1;
 }
 
 void dattn_store::fill_fused(const Plan& pl, MAParams& f) {
