@@ -26,6 +26,9 @@ def _port():
     return p
 
 
+MODES = {"k5_nvlink": {"DATTN_FUSED_MERGE": "1"}, "nccl": {"DATTN_FUSED_MERGE": "0"},
+         "k1_push_k6": {"DATTN_FUSED_MERGE": "1", "DATTN_FUSED_K1": "1"}}
+
 CASES = {
     "gqa_bf16": dict(lens=[5000, 37, 20000, 1, 16], hq=64, hkv=8, d=128, dtype=0, tol=2e-2),
     "mha_f32": dict(lens=[4096, 3, 777], hq=32, hkv=32, d=128, dtype=1, tol=1e-3),
@@ -43,7 +46,7 @@ def _worker(rank, world, port, case, placement, fused, q):
     from paper_2401_02669_b200.sharding import placement_from_moves, plan_rank_ranges
 
     try:
-        os.environ["DATTN_FUSED_MERGE"] = "1" if fused else "0"
+        os.environ.update(MODES[fused])
         torch.cuda.set_device(rank)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -76,7 +79,7 @@ def _worker(rank, world, port, case, placement, fused, q):
         st.decode_sharded(ranges, len(lens), qd, out)
         torch.cuda.synchronize()
         # fused: MA kernels push merged groups over NVLink (3) / K5 (2)
-        assert st.stats().last_exchange in ((2, 3) if fused else (1,))
+        assert st.stats().last_exchange == {"k5_nvlink": 2, "nccl": 1, "k1_push_k6": 3}[fused]
         # repeated back-to-back steps reuse the double-buffered exchange
         # (epoch flags): ranks may run a step ahead of each other
         for _ in range(20):
@@ -106,7 +109,7 @@ def _worker(rank, world, port, case, placement, fused, q):
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("case", sorted(CASES))
 @pytest.mark.parametrize("placement", [False, True])
-@pytest.mark.parametrize("fused", [True, False], ids=["k5_nvlink", "nccl"])
+@pytest.mark.parametrize("fused", sorted(MODES))
 def test_sharded_decode_matches_oracle(case, placement, fused):
     import torch.multiprocessing as mp
     world = min(_ngpus(), 4)

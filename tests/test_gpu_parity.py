@@ -250,18 +250,18 @@ def test_fused_group_merge_equals_separate_merge(torch_cuda, hq, hkv):
     rg = []
     for b, (s, L) in enumerate(zip(seqs, lens)):
         rg += [pb.Range(s, b, 0, L // 3), pb.Range(s, b, L // 3, L)]
-    fused = out_np(torch, decode(torch, st, rg, 7, q), 128)
-    assert st.stats().last_exchange == 0
-    os.environ["DATTN_FUSED_K1"] = "0"
+    os.environ["DATTN_FUSED_K1"] = "1"
     try:
-        sep = out_np(torch, decode(torch, st, rg, 7, q), 128)
+        fused = out_np(torch, decode(torch, st, rg, 7, q), 128)
+        assert st.stats().last_exchange == 0
+        again = out_np(torch, decode(torch, st, rg, 7, q), 128)
     finally:
         del os.environ["DATTN_FUSED_K1"]
+    sep = out_np(torch, decode(torch, st, rg, 7, q), 128)
     # bf16 outputs: fp32 re-association may flip the last bf16 bit
     assert rel_errs(fused[:6], sep[:6]) < 4e-3
     assert not fused[6].any() and not sep[6].any()  # row without ranges
     # repeated launches reuse the self-resetting completion counters
-    again = out_np(torch, decode(torch, st, rg, 7, q), 128)
     assert np.array_equal(again, fused)
 
 
