@@ -317,6 +317,10 @@ def run_b200_arm(args, rank, ws, local):
     ma_ms = s.ma_ms / max(s.ma_timed, 1)
     merge_ms = s.merge_ms / max(s.merge_timed, 1)
     comm_ms = s.comm_ms / max(s.comm_timed, 1) if s.comm_timed else None
+    rank_times = [[ma_ms, comm_ms]]
+    if ws > 1:
+        rank_times = [None] * ws
+        dist.all_gather_object(rank_times, [ma_ms, comm_ms])
     kernel_name = {1: "ma_decode_kernel (K1, CUDA cores)", 2: "gqa_tc_kernel (K2, tcgen05)"}.get(s.last_kernel, "?")
 
     # ---- region C: end to end through the C ABI with host buffers ----
@@ -372,6 +376,8 @@ def run_b200_arm(args, rank, ws, local):
         "e2e": {"value": w.batch / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": qbytes + plan_bytes,
                 "d2h_bytes_per_step": qbytes, "ms_per_step": t_e2e * 1e3},
         "gpu_launches": launches,
+        "per_rank_ms": {"ma": [round(t[0], 4) for t in rank_times],
+                        "exchange": [None if t[1] is None else round(t[1], 4) for t in rank_times]},
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:
