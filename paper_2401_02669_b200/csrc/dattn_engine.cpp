@@ -296,7 +296,34 @@ void dattn_store::grow(int32_t seq, int64_t tokens) {
 
 // ----------------------------------------------------------------- planner
 
-void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl) const {
+// Steady-state decode repeats the same batch: reuse the last plan when the
+// batch is identical (after re-checking the ranges against the ledger).
+void dattn_store::plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl) {
+    const size_t rbytes = static_cast<size_t>(std::max(b.num_ranges, 0)) * sizeof(dattn_range);
+    const bool same = plan_cached && cache_one_chunk == one_chunk_per_range && cache_rows == b.num_rows &&
+                      cache_chunk == b.chunk_tokens && b.num_ranges >= 0 && b.ranges != nullptr &&
+                      cache_ranges.size() == rbytes &&
+                      std::memcmp(cache_ranges.data(), b.ranges, rbytes) == 0;
+    if (same && &pl == &cache_plan) {
+        for (int i = 0; i < b.num_ranges; ++i) {
+            const dattn_range& r = b.ranges[i];
+            check_seq(r.seq);
+            if (r.tok_end > seq_tokens[r.seq]) throw Error(DATTN_ERR_CONTRACT, "range tokens outside the sequence");
+        }
+        return;
+    }
+    build_plan(b, one_chunk_per_range, pl);
+    if (&pl == &cache_plan) {
+        plan_cached = true;
+        cache_one_chunk = one_chunk_per_range;
+        cache_rows = b.num_rows;
+        cache_chunk = b.chunk_tokens;
+        cache_ranges.assign(reinterpret_cast<const unsigned char*>(b.ranges),
+                            reinterpret_cast<const unsigned char*>(b.ranges) + rbytes);
+    }
+}
+
+void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Plan& pl) const {
     if (b.num_rows < 0 || b.num_ranges < 0)
         throw Error(DATTN_ERR_INVALID_ARGUMENT, "negative row/range count");
     if (b.num_ranges > 0 && !b.ranges)
@@ -587,7 +614,7 @@ void dattn_store::check_flag() {
 void dattn_store::decode(const dattn_batch& b, const void* q, void* out, void* row_partials,
                          int mem) {
     activate();
-    Plan& pl = scratch_plan;
+    Plan& pl = cache_plan;
     plan(b, false, pl);
     upload_plan(pl);
     const bool want_out = out && !(b.flags & DATTN_F_NO_OUTPUT);
@@ -635,7 +662,7 @@ void dattn_store::decode(const dattn_batch& b, const void* q, void* out, void* r
 
 void dattn_store::micro_attention(const dattn_batch& b, const void* q_dev, void* partials) {
     activate();
-    Plan& pl = scratch_plan;
+    Plan& pl = cache_plan;
     plan(b, true, pl);
     upload_plan(pl);
     const bool check = (b.flags & DATTN_F_CHECK_FINITE) != 0;
@@ -652,7 +679,7 @@ void dattn_store::micro_attention(const dattn_batch& b, const void* q_dev, void*
 void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out, int mem) {
     if (!comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
     activate();
-    Plan& pl = scratch_plan;
+    Plan& pl = cache_plan;
     plan(b, false, pl);
     upload_plan(pl);
     const void* q_dev = q;

@@ -137,7 +137,12 @@ struct dattn_store {
     void write_rows(int32_t seq, int kv_head, int64_t tok0, int64_t n, const void* k,
                     const void* v, int src_dtype, int src_row_elems);
 
-    void plan(const dattn_batch& b, bool one_chunk_per_range, dattn::Plan& pl) const;
+    void plan(const dattn_batch& b, bool one_chunk_per_range, dattn::Plan& pl);
+    void build_plan(const dattn_batch& b, bool one_chunk_per_range, dattn::Plan& pl) const;
+    dattn::Plan cache_plan;
+    bool plan_cached = false, cache_one_chunk = false;
+    int32_t cache_rows = -1, cache_chunk = -1;
+    std::vector<unsigned char> cache_ranges;
     void upload_plan(const dattn::Plan& pl);
     void run_ma(const dattn::Plan& pl, const void* q_dev, void* recs, double scale,
                 bool check_finite, const dattn::MAParams* fused = nullptr);
