@@ -395,6 +395,12 @@ def test_contract_errors(torch_cuda):
         st.decode([pb.Range(s, 2, 0, 5)], 2, q, out)  # row out of bounds
     with pytest.raises(pb.ContractError):
         pb.Store(128, 6, 4, pb.BF16, 16, 16)
+    # the plan cache re-validates an identical batch against the ledger
+    st.decode([pb.Range(s, 0, 0, 10)], 1, q, out)
+    st.decode([pb.Range(s, 0, 0, 10)], 1, q, out)
+    st.seq_release(s)
+    with pytest.raises(pb.ContractError):
+        st.decode([pb.Range(s, 0, 0, 10)], 1, q, out)
 
 
 # ------------------------------------------------------ reference-facing API
