@@ -781,7 +781,7 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         // groups per CTA iteration: 8 when groups are plentiful, else 1 so few
         // heavy groups still spread over many CTAs -- a function of rows x heads
         // only, hence identical on every rank. Warps per group is a local choice.
-        const int64_t gpc = static_cast<int64_t>(row_recs) >= 16LL * num_sms ? 8 : 1;
+        const int64_t gpc = static_cast<int64_t>(row_recs) >= 1024 ? 8 : 1;
         xp.groups_per_cta = static_cast<int32_t>(gpc);
         xp.warps_per_group = (gpc == 1 || max_row_chunks > 64) ? 8 : 1;
         const int grid = static_cast<int>(std::max<int64_t>(
