@@ -7,6 +7,7 @@
 #include <array>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -153,6 +154,18 @@ void dattn_store::setup_exchange() {
 }
 
 dattn_store::~dattn_store() {
+    if (!k5_trace_log.empty()) {
+        // DATTN_K5_TRACE summary: mean over calls (first 3 skipped), us from the first CTA start
+        std::array<double, 6> m{};
+        size_t n = 0;
+        for (size_t i = 3; i < k5_trace_log.size(); ++i, ++n)
+            for (int j = 0; j < 6; ++j) m[j] += k5_trace_log[i][j];
+        if (n)
+            std::fprintf(stderr,
+                         "[K5 trace rank %d] calls %zu: start spread %.2f us, A(max) %.2f, fence+flags(max) %.2f, "
+                         "wait(max) %.2f, D(max) %.2f, last t0 %.0f ns\n",
+                         rank, n, m[0] / n, m[1] / n, m[2] / n, m[3] / n, m[4] / n, k5_trace_log.back()[5]);
+    }
     release_exchange();
     if (comm) ncclCommDestroy(comm);
     for (auto* v : {&ma_events, &merge_events, &comm_events})
@@ -787,10 +800,28 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,
                                  std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));
+        static const bool trace = std::getenv("DATTN_K5_TRACE") != nullptr;
+        if (trace) {
+            k5_trace.ensure(static_cast<size_t>(grid) * 5 * sizeof(unsigned long long));
+            xp.trace = static_cast<unsigned long long*>(k5_trace.p);
+        }
         cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
         if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
         cuda_check(launch_merge_exchange(cfg.dtype, dp, xp, grid, stream), "launch(K5 merge_exchange)");
         if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
+        if (trace) {
+            std::vector<unsigned long long> t(static_cast<size_t>(grid) * 5);
+            cuda_check(cudaMemcpyAsync(t.data(), k5_trace.p, t.size() * 8, cudaMemcpyDeviceToHost, stream), "trace");
+            cuda_check(cudaStreamSynchronize(stream), "trace");
+            unsigned long long t0 = ~0ull, t0x = 0, mx[5] = {0, 0, 0, 0, 0};
+            for (int c = 0; c < grid; ++c) {
+                t0 = std::min(t0, t[c * 5]);
+                t0x = std::max(t0x, t[c * 5]);
+                for (int j = 1; j < 5; ++j) mx[j] = std::max(mx[j], t[c * 5 + j]);
+            }
+            k5_trace_log.push_back({(t0x - t0) * 1e-3, (mx[1] - t0) * 1e-3, (mx[2] - t0) * 1e-3,
+                                    (mx[3] - t0) * 1e-3, (mx[4] - t0) * 1e-3, static_cast<double>(t0)});
+        }
         count_launch(1);
         stats.last_exchange = 2;
         if (mem == DATTN_MEM_HOST) {

@@ -684,6 +684,14 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     const Acc* R = static_cast<const Acc*>(p.recs);
+    auto stamp = [&](int i) {
+        if (x.trace && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            x.trace[blockIdx.x * 5 + i] = t;
+        }
+    };
+    stamp(0);
 
     // ---- A. local merge + push to every rank. Light groups (<= kHeavy chunk
     //      records) are merged by one warp each, in parallel; heavy groups by
@@ -829,11 +837,13 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     }
     // ---- B. publish: one fence for the CTA, one flag per destination rank
     __syncthreads();
+    stamp(1);
     if (threadIdx.x == 0) {
         __threadfence_system();
         for (int r = 0; r < x.nranks; ++r)
             st_release_sys(x.peer_flags[r] + static_cast<int64_t>(x.rank) * x.flag_stride + blockIdx.x, x.epoch);
     }
+    stamp(2);
     // ---- C. wait for this CTA index on every rank (bounded: a peer that
     //      never publishes must not wedge the GPU)
     if (threadIdx.x < x.nranks) {
@@ -848,6 +858,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
         }
     }
     __syncthreads();
+    stamp(3);
     // ---- D. rank merge of this CTA's groups, one warp per group
     //      (exchange data read past L1: it was written remotely)
     const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
@@ -894,6 +905,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
                 for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(tok2 != Acc(0) ? a2[sw][v] / e2 : Acc(0));
         }
     }
+    __syncthreads();
+    stamp(4);
 }
 
 // ------------------------------------------------------------------ K6
