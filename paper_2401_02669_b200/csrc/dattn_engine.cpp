@@ -111,6 +111,8 @@ void dattn_store::setup_exchange() {
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
     cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
+    // every exchange word starts empty (all ones, see XWord in dattn_merge.cuh)
+    cuda_check(cudaMemsetAsync(xbuf, 0xFF, xbytes, stream), "cudaMemset(exchange)");
     cudaIpcMemHandle_t hx, hf;
     cuda_check(cudaIpcGetMemHandle(&hx, xbuf), "cudaIpcGetMemHandle");
     cuda_check(cudaIpcGetMemHandle(&hf, xflags), "cudaIpcGetMemHandle");
@@ -143,7 +145,7 @@ void dattn_store::setup_exchange() {
         cuda_check(cudaIpcOpenMemHandle(&f, pf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
         peer_flags[r] = static_cast<uint32_t*>(f);
     }
-    // every rank has zeroed its flags before anyone can publish
+    // every rank has emptied its exchange buffer and zeroed its flags before anyone can publish
     nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, dh.p, 2 * kH, ncclUint8,
                              comm, stream),
                "ncclAllGather(barrier)");
@@ -162,9 +164,9 @@ dattn_store::~dattn_store() {
             for (int j = 0; j < 6; ++j) m[j] += k5_trace_log[i][j];
         if (n)
             std::fprintf(stderr,
-                         "[K5 trace rank %d] calls %zu: start spread %.2f us, A(max) %.2f, fence+flags(max) %.2f, "
-                         "wait(max) %.2f, D(max) %.2f, last t0 %.0f ns\n",
-                         rank, n, m[0] / n, m[1] / n, m[2] / n, m[3] / n, m[4] / n, k5_trace_log.back()[5]);
+                         "[K5 trace rank %d] calls %zu: start spread %.2f us, A done(max) %.2f, end(max) %.2f, "
+                         "last t0 %.0f ns\n",
+                         rank, n, m[0] / n, m[1] / n, m[4] / n, k5_trace_log.back()[5]);
     }
     release_exchange();
     if (comm) ncclCommDestroy(comm);

@@ -647,28 +647,28 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
 }
 
 // ------------------------------------------------------------------ K5
-// Fused cross-GPU merge: a persistent grid walks the (row, q
-// head) groups in the same order on every rank. For each group it merges this
-// rank's chunk records (as K3), stores the merged record straight into every
-// rank's exchange buffer over NVLink (peer pointers from CUDA IPC), publishes
-// it with a release store of the step epoch into the owner's flag, waits for
-// the flags of all ranks (acquire, system scope) and merges the nranks records
-// into the output. Replaces local K3 + ncclAllGather + rank K3.
-
-// A CTA owns groups [(blockIdx.x + k*gridDim.x)*gpc, +gpc) with gpc = 8/wpg
-// groups per iteration and wpg warps per group (1 for short chunk lists, 8
-// for long ones such as a 1M-token request). Phase A: the wpg warps of a group
-// merge its chunk records (max pass, then rescale-sum, combined through
-// shared memory in a fixed order) and store the result into every rank's
-// exchange buffer (NVLink stores for peers). Phase B: one system-scope fence
-// per CTA, then one release flag per (destination rank, CTA). Phase C: wait
-// for the same CTA index of every rank. Phase D: merge the nranks records of
-// the CTA's groups into the output. All ranks launch the same grid and group
-// order and the grid is co-resident, so the waits cannot deadlock.
+// Fused cross-GPU merge, one launch per step replacing local
+// K3 + ncclAllGather + rank K3. Phase A: every (row, q head) group's chunk
+// records on this rank are merged (as K3) and the merged record is stored
+// straight into every rank's exchange buffer (NVLink stores through CUDA IPC
+// peer pointers). Phase D: every group's nranks records are read back as they
+// arrive -- exchange words are self-validating (XWord: an empty word is the
+// all-ones NaN), so there is no fence, flag or barrier between the phases --
+// merged into the output, and the slots are emptied for the step after next.
+//
+// Phase A walks the groups in sweeps of gridDim.x * gpc; within a sweep CTA b
+// takes groups b, b + gridDim.x, ... so the consecutive heavy groups of one
+// long request (more than kHeavy chunk records each) land on different CTAs.
+// Light groups are merged by one warp each, heavy groups by the whole CTA.
+// Identity groups (no tokens on this rank) push only their header; a receiver
+// reads the payload of live records only, so every word written is read and
+// emptied exactly once. The grid is co-resident (<= 4 CTAs per SM), so a warp
+// spinning in phase D never starves a CTA still in phase A.
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const XParams x) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
+    using U = typename XWord<Acc>::U;
     constexpr int REC = DP + 4;
     constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
                                            : (DP % 64 == 0 ? 2 : 1);
@@ -693,9 +693,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     };
     stamp(0);
 
-    // ---- A. local merge + push to every rank. Light groups (<= kHeavy chunk
-    //      records) are merged by one warp each, in parallel; heavy groups by
-    //      the whole CTA, one after the other.
+    // ---- A. local merge + push to every rank
     constexpr int kHeavy = 64;
     auto group_shape = [&](int64_t g, int& n, int& cbase, int64_t& base, int& my_kvh) {
         const int row = static_cast<int>(g / p.heads);
@@ -707,32 +705,33 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     };
     auto push = [&](int64_t g, const Acc (&acc)[kSweeps][kVW], Acc mg, Acc eg, Acc ntok) {
         const int64_t slot = (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
+        const U hdr[4] = {x_enc(ntok != Acc(0) ? mg : kNegInf), x_enc(eg), x_enc(ntok), x_enc(Acc(0))};
         for (int r = 0; r < x.nranks; ++r) {
-            Acc* dst = static_cast<Acc*>(x.peer_x[r]) + slot;
+            U* dst = static_cast<U*>(x.peer_x[r]) + slot;
+            if (ntok != Acc(0)) {
 #pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP)
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP) {
+                        U w[kVW];
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) dst[4 + j + v] = acc[sw][v];
+                        for (int v = 0; v < kVW; ++v) w[v] = x_enc(acc[sw][v]);
+                        x_store<U, kVW>(dst + 4 + j, w);
+                    }
+                }
             }
-            if (lane == 0) {
-                dst[0] = ntok != Acc(0) ? mg : kNegInf;
-                dst[1] = eg;
-                dst[2] = ntok;
-                dst[3] = 0;
-            }
+            if (lane == 0) x_store<U, 4>(dst, hdr);
         }
     };
-    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
-         gb += static_cast<int64_t>(gridDim.x) * gpc) {
-        // light groups: warp w takes group gb + w
-        if (warp < gpc && gb + warp < groups) {
-            const int64_t g = gb + warp;
-            int n, cbase, my_kvh;
-            int64_t base;
-            group_shape(g, n, cbase, base, my_kvh);
-            if (n <= kHeavy) {
+    const int64_t sweep = static_cast<int64_t>(gridDim.x) * gpc;
+    for (int64_t gb = 0; gb < groups; gb += sweep) {
+        // light groups: warp w takes group gb + w * gridDim.x + blockIdx.x
+        if (warp < gpc) {
+            const int64_t g = gb + static_cast<int64_t>(warp) * gridDim.x + blockIdx.x;
+            int n = 0, cbase = 0, my_kvh = 0;
+            int64_t base = 0;
+            if (g < groups) group_shape(g, n, cbase, base, my_kvh);
+            if (g < groups && n <= kHeavy) {
                 auto live = [&](int c, const Acc* r) {
                     if (p.chunk_kvh) {
                         const int tag = p.chunk_kvh[cbase + c];
@@ -762,7 +761,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
         }
         // heavy groups: the whole CTA, 8 warps striding over the chunk records
         for (int rep = 0; rep < gpc; ++rep) {
-            const int64_t g = gb + rep;
+            const int64_t g = gb + static_cast<int64_t>(rep) * gridDim.x + blockIdx.x;
             if (g >= groups) break;
             int n, cbase, my_kvh;
             int64_t base;
@@ -835,65 +834,63 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             __syncthreads();
         }
     }
-    // ---- B. publish: one fence for the CTA, one flag per destination rank
-    __syncthreads();
     stamp(1);
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (int r = 0; r < x.nranks; ++r)
-            st_release_sys(x.peer_flags[r] + static_cast<int64_t>(x.rank) * x.flag_stride + blockIdx.x, x.epoch);
-    }
-    stamp(2);
-    // ---- C. wait for this CTA index on every rank (bounded: a peer that
-    //      never publishes must not wedge the GPU)
-    if (threadIdx.x < x.nranks) {
-        const uint32_t* f = x.peer_flags[x.rank] + static_cast<int64_t>(threadIdx.x) * x.flag_stride + blockIdx.x;
-        uint64_t t0 = 0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        while (ld_acquire_sys(f) != x.epoch) {
-            __nanosleep(32);
-            uint64_t t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 10000000000ull) __trap();
+
+    // ---- D. rank merge, one warp per group: lane r reads rank r's header,
+    //      every lane its payload words of each live record, in rank order
+    U* X = static_cast<U*>(x.peer_x[x.rank]);
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
+         g += static_cast<int64_t>(gridDim.x) * kMergeWarps) {
+        Acc mr = kNegInf, er = 0, tr = 0;
+        if (lane < x.nranks) {
+            U h[4];
+            x_poll<U, 4>(X + (static_cast<int64_t>(lane) * x.slot_stride + g) * REC, h);
+            mr = x_dec<Acc>(h[0]);
+            er = x_dec<Acc>(h[1]);
+            tr = x_dec<Acc>(h[2]);
         }
-    }
-    __syncthreads();
-    stamp(3);
-    // ---- D. rank merge of this CTA's groups, one warp per group
-    //      (exchange data read past L1: it was written remotely)
-    const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
-    for (int64_t gb = static_cast<int64_t>(blockIdx.x) * gpc; gb < groups;
-         gb += static_cast<int64_t>(gridDim.x) * gpc) {
-        if (warp >= gpc) continue;
-        const int64_t g = gb + warp;
-        if (g >= groups) continue;
-        Acc m2 = kNegInf;
-        for (int r = lane; r < x.nranks; r += 32) {
-            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
-        }
+        Acc m2 = tr != Acc(0) ? mr : kNegInf;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, off));
+        const Acc wl = tr != Acc(0) ? ((mr == m2) ? Acc(1) : exp(mr - m2)) : Acc(0);
         Acc e2 = 0, tok2 = 0;
         Acc a2[kSweeps][kVW];
 #pragma unroll
         for (int sw = 0; sw < kSweeps; ++sw)
 #pragma unroll
             for (int v = 0; v < kVW; ++v) a2[sw][v] = 0;
+        unsigned live_mask = 0;
         for (int r = 0; r < x.nranks; ++r) {
-            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            const Acc tk = __ldcv(rec + 2);
-            if (tk == Acc(0)) continue;
-            const Acc mr = __ldcv(rec);
-            const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
-            e2 += __ldcv(rec + 1) * w;
+            const Acc tk = __shfl_sync(0xffffffffu, tr, r);
+            const Acc w = __shfl_sync(0xffffffffu, wl, r);
+            const Acc er_r = __shfl_sync(0xffffffffu, er, r);
+            if (tk == Acc(0)) continue;  // warp-uniform
+            live_mask |= 1u << r;
+            e2 += er_r * w;
             tok2 += tk;
+            const U* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
 #pragma unroll
             for (int sw = 0; sw < kSweeps; ++sw) {
                 const int j = sw * kPer + lane * kVW;
-                if (j < DP)
+                if (j < DP) {
+                    U d[kVW];
+                    x_poll<U, kVW>(rec + 4 + j, d);
 #pragma unroll
-                    for (int v = 0; v < kVW; ++v) a2[sw][v] += __ldcv(rec + 4 + j + v) * w;
+                    for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(d[v]) * w;
+                }
+            }
+        }
+        __syncwarp();
+        // empty the slots for the step after next
+        for (int r = 0; r < x.nranks; ++r) {
+            U* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            if (lane == r) x_clear<U, 4>(rec);
+            if (live_mask & (1u << r)) {
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw) {
+                    const int j = sw * kPer + lane * kVW;
+                    if (j < DP) x_clear<U, kVW>(rec + 4 + j);
+                }
             }
         }
         T* o = static_cast<T*>(x.out_norm) + g * DP;
@@ -1000,6 +997,14 @@ __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const Rank
                 const int j = lane + 32 * k;
                 if (j < DP) a2[k] += __ldcv(rec + 4 + j) * w;
             }
+        }
+        // empty the slots (the all-ones word K5 reads as "not arrived"): the
+        // delivered counters already proved every word landed
+        __syncwarp();
+        using U = typename XWord<Acc>::U;
+        for (int r = 0; r < x.nranks; ++r) {
+            U* rec = reinterpret_cast<U*>(const_cast<Acc*>(X)) + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
+            for (int j = lane; j < REC; j += 32) rec[j] = ~U(0);
         }
         T* o = static_cast<T*>(x.out_norm) + g * DP;
 #pragma unroll

@@ -5,6 +5,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 #include "dattn_internal.h"
 #include "dattn_ptx.cuh"
@@ -73,6 +74,85 @@ __device__ __forceinline__ void fold_chunks(const Acc* R, int64_t base, int64_t 
     ntok = t_l;
 }
 
+
+// ---- exchange slots without flags (K5). An exchange word that has not
+// arrived holds all ones -- a NaN no arithmetic produces, and producers map
+// that one bit pattern to the payload-less NaN below -- so a receiver sees a
+// word arrive from its value alone: no system fence, no flag, no second
+// NVLink round trip. The receiver puts the empty pattern back after reading,
+// which is safe because a peer writes the same half of the buffer again only
+// two steps later, after it has seen this rank's next-step records.
+template <class Acc> struct XWord;
+template <> struct XWord<float> { using U = uint32_t; };
+template <> struct XWord<double> { using U = unsigned long long; };
+
+template <class Acc>
+__device__ __forceinline__ typename XWord<Acc>::U x_enc(Acc v) {
+    using U = typename XWord<Acc>::U;
+    U b;
+    memcpy(&b, &v, sizeof b);
+    return b == ~U(0) ? (~U(0) >> 1) : b;
+}
+template <class Acc>
+__device__ __forceinline__ Acc x_dec(typename XWord<Acc>::U b) {
+    Acc v;
+    memcpy(&v, &b, sizeof v);
+    return v;
+}
+
+// N words at p (16-byte aligned when N*sizeof(U) is a multiple of 16)
+template <class U, int N>
+__device__ __forceinline__ void x_store(U* p, const U (&w)[N]) {
+    if constexpr ((N * sizeof(U)) % 16 == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i += 16 / sizeof(U))
+            *reinterpret_cast<uint4*>(p + i) = *reinterpret_cast<const uint4*>(&w[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) p[i] = w[i];
+    }
+}
+template <class U, int N>
+__device__ __forceinline__ void x_clear(U* p) {
+    U w[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = ~U(0);
+    x_store<U, N>(p, w);
+}
+__device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
+// Spin until none of the N words is empty (bounded: a peer that never
+// delivers traps after 10 s instead of wedging the GPU).
+template <class U, int N>
+__device__ __forceinline__ void x_poll(const U* p, U (&w)[N]) {
+    uint64_t t0 = 0;
+    for (int spin = 0;; ++spin) {
+        bool ok = true;
+        if constexpr ((N * sizeof(U)) % 16 == 0) {
+#pragma unroll
+            for (int i = 0; i < N; i += 16 / sizeof(U)) {
+                const uint4 v = ld_volatile_v4(p + i);
+                *reinterpret_cast<uint4*>(&w[i]) = v;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) w[i] = *reinterpret_cast<const volatile U*>(p + i);
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) ok &= (w[i] != ~U(0));
+        if (ok) return;
+        if ((spin & 255) == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (spin == 0) t0 = t;
+            else if (t - t0 > 10000000000ull) __trap();
+        }
+    }
+}
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
