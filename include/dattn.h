@@ -240,13 +240,17 @@ typedef struct dattn_merge_desc {
 dattn_status dattn_merge_partials(dattn_store* s, const dattn_merge_desc* d, const void* recs,
                                   void* out_recs, void* out_norm);
 
-/* ------------------------------------------------ multi-GPU (NCCL merge) */
+/* ------------------------------------------------ multi-GPU (NVLink merge) */
 
 /* Sequence-sharded decode across the GPUs of one box: every
- * rank holds its rBlocks of each request, runs K1 + local K3 into one partial
- * per (row, q head), ncclAllGather's the packed records over NVLink and
- * merges them with K3 -- the paper's "(o, m, l)" exchange
- * replacing the simulated remote-partial latency of simengine.cpp:397-407. */
+ * rank holds its rBlocks of each request, runs the MA kernel over them, merges
+ * them into one partial per (row, q head), stores that record into every
+ * rank's exchange buffer over NVLink (CUDA IPC peer memory set up by
+ * dattn_comm_init) and merges the nranks records into out -- the paper's
+ * "(o, m, l)" exchange replacing the simulated
+ * remote-partial latency of simengine.cpp:397-407. Every rank gets the full
+ * output. DATTN_FUSED_MERGE=0 in the environment selects ncclAllGather of the
+ * records instead. */
 #define DATTN_UNIQUE_ID_BYTES 128
 dattn_status dattn_comm_unique_id(unsigned char id[DATTN_UNIQUE_ID_BYTES]);
 dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE_ID_BYTES],

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = p.group;
+    pdl_launch_dependents();  // the merge launch may queue up behind this grid
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kKStages; ++i) {

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     constexpr int TS = S::kStageTokens, U = S::kUnroll, REC = S::kRec;
 
     extern __shared__ __align__(128) uint8_t smem[];
+    pdl_launch_dependents();  // the merge launch may queue up behind this grid
     const Layout<T, DP> L(p.stages, p.group);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + p.stages;
@@ -561,6 +562,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
     __shared__ Acc s_tok[kMergeWarps];
     __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
 
+    pdl_wait();  // launched early behind the MA grid (PDL)
     const int64_t g = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = static_cast<int>(g / p.heads);
@@ -683,6 +685,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     const int gpc = x.groups_per_cta;  // 1 or kMergeWarps; identical on every rank
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
+    pdl_wait();  // launched early behind the MA grid (PDL)
     const Acc* R = static_cast<const Acc*>(p.recs);
     auto stamp = [&](int i) {
         if (x.trace && threadIdx.x == 0) {
@@ -1247,12 +1250,30 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
     return cudaLaunchKernel(f, dim3(grid), dim3(kMAThreads), args, smem, st);
 }
 
+// launch with programmatic stream serialization: the kernel is scheduled
+// while the previous grid on the stream drains and waits in pdl_wait()
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st) {
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     if (groups == 0) return cudaSuccess;
     const int grid = static_cast<int>(groups);
-    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (e = launch_pdl(merge_kernel<TC, DPC>, grid, 32 * kMergeWarps, st, p))));
+    return e;
 }
 
 static int grid_for(int64_t total) {
@@ -1262,8 +1283,9 @@ static int grid_for(int64_t total) {
 }
 
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st) {
-    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (merge_exchange_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
-    return cudaGetLastError();
+    cudaError_t e = cudaSuccess;
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (e = launch_pdl(merge_exchange_kernel<TC, DPC>, grid, 32 * kMergeWarps, st, p))));
+    return e;
 }
 
 cudaError_t launch_rank_merge(int dtype, int dp, const RankMergeParams& p, int grid, cudaStream_t st) {
