@@ -4,19 +4,29 @@
 Default workload: BASELINE config 2 (batch 64 decode, LLaMA2-7B MHA 32x128,
 ragged 1K-32K contexts, bf16 paged KV) on 1 B200. With --gpus N (launched by
 torch.distributed.run, one process per GPU) the SAME workload is
-sequence-sharded: every request's blocks are split into N contiguous shares,
-each rank runs K1 + its local K3 merge and the (m, e, ma) partials are merged
-across ranks with one ncclAllGather + K3 (strong scaling, total work fixed).
+sequence-sharded: every request's blocks are split into N contiguous shares
+(config 5: the gManager-policy placement), each rank runs the MA kernel over its
+share and K5 merges the (m, e, ma) partials locally, exchanges one record per
+(row, q head) over NVLink and merges across ranks (strong scaling, total work
+fixed).
 
 A step = one decode step of one attention layer for the whole batch.
   value       tokens/s = B / t_step, inputs resident in HBM, device-timed with
               CUDA events over exactly --steps steps (max over ranks).
   e2e         the same through the C ABI with HOST q/out buffers: pinned H2D of
               q + plan, D2H of the output inside every step (wall clock).
-  roofline    K1 (the MA kernel, the dominant launch) timed alone with CUDA
-              events on its stream; achieved = algorithmic bytes / duration.
+  roofline    the MA kernel (K1 or K2, the dominant launch) timed alone with
+              CUDA events on its stream; achieved = algorithmic bytes / duration;
+              frac against the measured copy bandwidth, frac_nominal against
+              the north_star's 8 TB/s.
+  placement   per-rank KV bytes, the makespan bound they imply (max rank bytes
+              at the measured peak) and the step's fraction of it (config 5 is
+              placement-limited).
   cpu_baseline the reference's own multi_head_attention (oracle/_ref, compiled
-              from the unmodified sources) on the host cores, bounded sample.
+              from the unmodified sources) on all host cores, bounded sample;
+              single_thread_value = the same on 1 core (as shipped).
+  model_tps   B / (n_layers * t_step), the reference's TPS = beta/(n T_layer)
+              (perfmodel.cpp:120-130) for the workload's model depth.
 --impl reference times only that CPU reference (rank 0) and prints its line.
 """
 from __future__ import annotations
@@ -346,6 +356,8 @@ def run_b200_arm(args, rank, ws, local):
     peak, peak_src = measured_peak()
     # per-rank algorithmic bytes of one K1 launch (rank 0's share)
     kv_rank = sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in shares)
+    kv_ranks = [sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in rs) for rs in workloads.rank_shares(w, ws)]
+    bound_ms = max(kv_ranks) / (peak * 1e9) * 1e3
     alg_rank = kv_rank + w.batch * w.hq * w.d * 2 * w.elem_bytes
     achieved = alg_rank / (ma_ms * 1e-3) / 1e9
     traffic = None
@@ -368,10 +380,13 @@ def run_b200_arm(args, rank, ws, local):
                    else "KV near L2 size: steps re-read it (L2-warm)",
                    "chunk_tokens": s.last_chunk_tokens, "ma_items": s.last_items, "ma_grid": s.ma_grid, **w.meta},
         "kv_gbs": w.kv_bytes() / (ms_step * 1e-3) / 1e9,
+        "model_tps": {"value": value / w.n_layers, "n_layers": w.n_layers},
         "rank0_kv_bytes": kv_rank,
+        "placement": {"per_rank_kv_bytes": kv_ranks, "bound_ms": bound_ms, "frac": bound_ms / ms_step,
+                      "aggregate_frac": w.kv_bytes() / (ws * peak * 1e9) / (ms_step * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": kernel_name, "kernel_ms": ma_ms, "merge_ms": merge_ms, "allgather_ms": comm_ms,
+                     "frac": achieved / peak, "traffic": traffic, "frac_nominal": achieved / 8000.0,
+                     "kernel": kernel_name, "kernel_ms": ma_ms, "merge_ms": merge_ms, "exchange_ms": comm_ms,
                      "alg_bytes_per_launch": alg_rank, "peak_source": peak_src},
         "e2e": {"value": w.batch / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": qbytes + plan_bytes,
                 "d2h_bytes_per_step": qbytes, "ms_per_step": t_e2e * 1e3},
@@ -382,8 +397,11 @@ def run_b200_arm(args, rank, ws, local):
     }
     if ws == 1 and not args.no_cpu_baseline:
         cv, info = cpu_reference_sample(w, args.cpu_seconds)
+        c1, info1 = cpu_reference_sample(w, min(args.cpu_seconds, 4.0), threads=1)
         line["cpu_baseline"] = {"value": cv, "unit": "tokens/s", "cores": info["cores"], "kind": info["kind"],
-                                "sample": info["sample"] + f"; {info['reps']} reps"}
+                                "sample": info["sample"] + f"; {info['reps']} reps",
+                                "single_thread_value": c1, "single_thread_reps": info1["reps"],
+                                "kv_gbs_fp64": info["kv_gbs_fp64"], "single_thread_kv_gbs_fp64": info1["kv_gbs_fp64"]}
     print(json.dumps(line), flush=True)
 
 

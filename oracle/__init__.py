@@ -247,9 +247,42 @@ def ref():
             "ref_rng_draws": [U64, ctypes.c_int, VP, VP, VP, VP, I64, I64],
             "ref_decode_timed": [ctypes.c_int, VP, VP, VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, D,
                                  I64, ctypes.c_int, VP, VP],
+            "ref_default_config_json": [ctypes.c_int, I64, ctypes.POINTER(ctypes.c_void_p)],
+            "ref_config_eval": [ctypes.c_char_p, ctypes.c_int, VP, VP, I64, VP, VP, VP],
         }.items():
             f = getattr(r, n)
             f.restype = ctypes.c_int
             f.argtypes = a
         _ref = r
     return _ref
+
+
+# ---- the reference perf model / config ----
+def ref_default_config(n_instances: int = 4, capacity_blocks: int = 256) -> str:
+    """The reference's default cluster config (config.cpp:71-87) as JSON text."""
+    r = ref()
+    p = ctypes.c_void_p()
+    rc = r.ref_default_config_json(n_instances, capacity_blocks, ctypes.byref(p))
+    if rc != 0:
+        raise RuntimeError(r.ref_last_error().decode())
+    try:
+        return ctypes.string_at(p).decode()
+    finally:
+        r.ref_string_free.argtypes = [ctypes.c_void_p]
+        r.ref_string_free(p)
+
+
+def ref_config_eval(text: str, xs: Sequence[float], ctx_lengths: Sequence[int]):
+    """Parse ``text`` with the reference parser (which validates every curve)
+    and return (g(xs), layer_time(load of ctx_lengths), n_layers). Raises
+    ValueError with the reference's message when the config is rejected."""
+    r = ref()
+    x = np.ascontiguousarray(xs, dtype=np.float64)
+    g = np.zeros(len(x))
+    L = np.ascontiguousarray(ctx_lengths, dtype=np.int64)
+    lt = np.zeros(1)
+    nl = np.zeros(1, dtype=np.int32)
+    rc = r.ref_config_eval(text.encode(), len(x), _p(x), _p(g), len(L), _p(L), _p(lt), _p(nl))
+    if rc != 0:
+        raise ValueError(r.ref_last_error().decode())
+    return g, float(lt[0]), int(nl[0])

@@ -4,10 +4,15 @@
 // (kvsched::attn in /root/reference/proj/src/distattention.cpp, verify.cpp,
 // trace.cpp), compiled together by oracle/Makefile into
 // oracle/_ref/libkvsched_ref.so. Used to (1) pin the C restatement in
-// dattn_oracle.c (tests/golden/make_golden.py) and (2) time the reference CPU
-// path for bench.py --impl reference / cpu_baseline.
+// dattn_oracle.c (tests/golden/make_golden.py), (2) time the reference CPU
+// path for bench.py --impl reference / cpu_baseline and (3) check that a
+// ctx_rate_curve measured on the B200 (tools/calibrate_ctx_curve.py, SURVEY
+// §8f row 4) is accepted by the reference's own config parser and perf model
+// (perfmodel.cpp, config.cpp).
 #include "kvsched/common.hpp"
+#include "kvsched/config.hpp"
 #include "kvsched/distattention.hpp"
+#include "kvsched/perfmodel.hpp"
 #include "kvsched/trace.hpp"
 #include "kvsched/verify.hpp"
 
@@ -234,6 +239,35 @@ int ref_decode_timed(int B, const int64_t* lens, const double* const* kv_ptrs,
         for (int i = 0; i < std::max(1, threads); ++i) pool.emplace_back(worker);
         for (auto& t : pool) t.join();
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// The reference's default cluster config as JSON (config.cpp:71-87 +
+// format_cluster_config); *out is malloc'ed, freed with ref_string_free.
+int ref_default_config_json(int n_instances, int64_t capacity_blocks, char** out) {
+    return guarded([&] {
+        const std::string j = sim::format_cluster_config(sim::default_cluster_config(n_instances, capacity_blocks));
+        *out = static_cast<char*>(std::malloc(j.size() + 1));
+        std::memcpy(*out, j.c_str(), j.size() + 1);
+    });
+}
+
+void ref_string_free(char* p) { std::free(p); }
+
+// Parse a cluster config with the reference parser (parse_cluster_config,
+// config.cpp:111-183, which validates every curve) and evaluate its
+// ctx_rate_curve g and the perf model's layer_time (perfmodel.cpp:105-113)
+// for a load of `batch` requests of the given context lengths.
+int ref_config_eval(const char* text, int n_x, const double* x, double* g_out, int64_t batch,
+                    const int64_t* ctx_lengths, double* layer_time_out, int* n_layers_out) {
+    return guarded([&] {
+        const sim::ClusterConfig c = sim::parse_cluster_config(text);
+        for (int i = 0; i < n_x; ++i) g_out[i] = c.g.eval(x[i]);
+        perf::InstanceLoad load;
+        load.batch = batch;
+        load.ctx_lengths.assign(ctx_lengths, ctx_lengths + batch);
+        *layer_time_out = perf::layer_time(load, c.shape, c.f, c.g);
+        *n_layers_out = c.shape.n_layers;
     });
 }
 

@@ -45,6 +45,7 @@ class Workload:
     amp_v: float = 2.0
     note: str = ""
     placement: str = "equal"  # "equal": plan_rank_ranges; "planner": planner_placement
+    n_layers: int = 32  # model depth for model-equivalent TPS (7B: 32, 70B: 80)
     meta: dict = field(default_factory=dict)
 
     @property
@@ -80,7 +81,7 @@ def config(name: str) -> Workload:
         return Workload("cfg2: batch 64 decode, LLaMA2-7B MHA 32x128, ragged 1K-32K, bf16 paged KV",
                         lens, 32, 32, 128, 0, meta={"lens_seed": seed, "lens_rule": "counter_uniform_int U[1024,32768]"})
     if name in ("3", "cfg3"):
-        return Workload("cfg3: LLaMA2-70B GQA 64q/8kv x128, batch 16 x 128K, bf16", [131072] * 16, 64, 8, 128, 0)
+        return Workload("cfg3: LLaMA2-70B GQA 64q/8kv x128, batch 16 x 128K, bf16", [131072] * 16, 64, 8, 128, 0, n_layers=80)
     if name in ("4", "cfg4"):
         return Workload("cfg4: 1 req x 1M tokens, LLaMA-7B MHA 32x128, bf16", [1048576], 32, 32, 128, 0)
     if name in ("5", "cfg5"):
