@@ -20,7 +20,7 @@ from dataclasses import dataclass
 from typing import Iterable, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdattn.so")
+LIB_PATH = os.environ.get("DATTN_LIB") or os.path.join(_HERE, "_lib", "libdattn.so")  # DATTN_LIB: A/B builds
 
 BF16, F32, F64 = 0, 1, 2
 MEM_DEVICE, MEM_HOST = 0, 1

@@ -368,7 +368,10 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     } else if (b.chunk_tokens > 0) {
         C = b.chunk_tokens;
     } else {
-        const int64_t target = static_cast<int64_t>(num_sms) * ma_ctas_per_sm * 12;
+        // ~12 items per CTA for K1; ~6 for K2, whose items cost a pipeline
+        // drain each (measured: 2048-token chunks 2-3% slower than 4096 at the
+        // same wave count, 1024-token chunks 8%)
+        const int64_t target = static_cast<int64_t>(num_sms) * ma_ctas_per_sm * (tc_ok ? 6 : 12);
         int64_t c = std::max<int64_t>(work / std::max<int64_t>(target, 1), 1);
         int64_t p2 = 1;
         while (p2 * 2 <= c) p2 *= 2;
