@@ -264,6 +264,7 @@ def run_b200_arm(args, rank, ws, local):
         cuts = [rr.tokens * i // nb for i in range(nb + 1)]
         for a, b in zip(cuts[:-1], cuts[1:]):
             ranges.append(pb.Range(seq, rr.request, a, b))
+    ranges = pb.range_array(ranges)  # packed once, reused by every step
     tdt = {0: torch.bfloat16, 1: torch.float32}[w.dtype]
     q = torch.empty(w.batch, w.hq, st.padded_dim, dtype=tdt, device=f"cuda:{local}")
     st.q_fill_synthetic(q, w.batch, w.seed, 0, 1.0)

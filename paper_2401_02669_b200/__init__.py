@@ -70,7 +70,7 @@ class Range(ctypes.Structure):
     output row ``out_row`` (kv_head -1: every kv head)."""
     _fields_ = [
         ("seq", ctypes.c_int32), ("out_row", ctypes.c_int32), ("kv_head", ctypes.c_int32),
-        ("last_exchange", ctypes.c_int32), ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64),
+        ("reserved", ctypes.c_int32), ("tok_begin", ctypes.c_int64), ("tok_end", ctypes.c_int64),
     ]
 
     def __init__(self, seq=0, out_row=0, tok_begin=0, tok_end=0, kv_head=-1):
@@ -237,7 +237,27 @@ def padded_dim(head_dim: int) -> int:
     raise ContractError(ERR_CONTRACT, "head_dim must be <= 256")
 
 
-def _batch(ranges: Sequence[Range], num_rows: int, chunk_tokens: int, flags: int, scale: float):
+class RangeArray:
+    """Ranges packed once into a ctypes array; decode calls accept it as-is,
+    so a decode loop over a fixed batch skips the per-call packing."""
+    __slots__ = ("arr", "n")
+
+    def __init__(self, ranges: Sequence[Range]):
+        self.n = len(ranges)
+        self.arr = (Range * max(self.n, 1))(*ranges)
+
+    def __len__(self):
+        return self.n
+
+
+def range_array(ranges: Sequence[Range]) -> RangeArray:
+    return RangeArray(ranges)
+
+
+def _batch(ranges, num_rows: int, chunk_tokens: int, flags: int, scale: float):
+    if isinstance(ranges, RangeArray):
+        b = Batch(num_rows, ranges.n, ctypes.cast(ranges.arr, ctypes.POINTER(Range)), chunk_tokens, flags, scale)
+        return b, ranges
     arr = (Range * max(len(ranges), 1))(*ranges)
     b = Batch(num_rows, len(ranges), ctypes.cast(arr, ctypes.POINTER(Range)), chunk_tokens, flags, scale)
     return b, arr

@@ -97,3 +97,15 @@ def test_struct_layouts_match_header(tmp_path):
                                        pb.MergeDesc)]
     want += [pb.Range.tok_begin.offset, pb.Batch.scale.offset, pb.StoreConfig.num_pages.offset]
     assert got == want
+
+
+def test_range_array_packs_like_a_list():
+    import paper_2401_02669_b200 as pb
+    rs = [pb.Range(3, 0, 5, 77), pb.Range(4, 1, 0, 1000, kv_head=2)]
+    a, _ = pb._batch(rs, 2, 0, 0, 0.0)
+    b, _ = pb._batch(pb.range_array(rs), 2, 0, 0, 0.0)
+    assert a.num_ranges == b.num_ranges == 2
+    for i in range(2):
+        x, y = a.ranges[i], b.ranges[i]
+        assert (x.seq, x.out_row, x.kv_head, x.tok_begin, x.tok_end) == (y.seq, y.out_row, y.kv_head, y.tok_begin, y.tok_end)
+    assert pb._batch(pb.range_array([]), 1, 0, 0, 0.0)[0].num_ranges == 0
