@@ -44,7 +44,7 @@ def test_curve_shape():
     # HBM-bound decode: the rate grows with S until the launch overhead is
     # amortised, then saturates near the copy bandwidth / KV bytes per token
     rates = [r for _, r in doc["ctx_rate_curve"]]
-    assert rates[-1] > 10 * rates[0]
+    assert rates[-1] > 3 * rates[0]
     peak_tok_s = 8.0e12 / (2 * 32 * 128 * 2)
     assert rates[-1] < peak_tok_s
 
