@@ -431,10 +431,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         float m[GI], l[GI], acc[GI], corr_prev[GI];
         bool pending = false;  // an O^T tile of the current item not yet accumulated
         float* recs = static_cast<float*>(p.records);
+        // An item's last O^T tile is still in the tensor pipe when its softmax
+        // is done; rather than wait for it, the item is finished one tile
+        // later, after the next item's first P^T has been handed to the MMA
+        // warp, so item boundaries do not drain the pipeline.
+        bool fin = false;
+        float fin_acc[GI], fin_corr[GI], fin_m[GI], fin_l[GI];
+        uint32_t fin_ob = 0, fin_oph = 0;
+        int64_t fin_rec0 = 0;
+        float fin_ntok = 0.f;
+        int fin_row = 0, fin_kvh = 0;
+        auto finish = [&]() {
+            mbar_wait(&S.o_full[fin_ob], fin_oph);
+            tc_fence_after();
+            float o[GI];
+            tmem_ld<GI>(tmem_o0 + fin_ob * kN + lane_addr, o);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.o_free[fin_ob]);
+#pragma unroll
+            for (int h = 0; h < GI; ++h) fin_acc[h] = fin_acc[h] * fin_corr[h] + o[h];
+            // e = sum over the 128 token rows of l
+#pragma unroll
+            for (int h = 0; h < GI; ++h) {
+                float v = fin_l[h];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) S.red_sum[ew][h] = v;
+            }
+            named_bar_sync(1, 128);
+#pragma unroll
+            for (int h = 0; h < GI; ++h) {
+                if (h >= G) continue;
+                float* rec = recs + (fin_rec0 + h) * (kD + 4);
+                rec[4 + row] = fin_acc[h];
+                if (row == 0) {
+                    rec[0] = fin_m[h] * 0.6931471805599453f;
+                    rec[1] = (S.red_sum[0][h] + S.red_sum[1][h]) + (S.red_sum[2][h] + S.red_sum[3][h]);
+                    rec[2] = fin_ntok;
+                    rec[3] = 0.f;
+                }
+            }
+            named_bar_sync(1, 128);
+            if (p.fused_mode != 0 && warp == 2 && lane == 0) {
+                // group completion (see K1): the CTA that wrote the last
+                // chunk of (row, kv head) hands it to the merge warp
+                const int gi = fin_row * p.num_kv_heads + fin_kvh;
+                const int old = atomic_add_acq_rel_gpu(p.group_counter + gi, 1);
+                if (old + 1 == __ldg(p.group_expected + gi)) {
+                    p.group_counter[gi] = 0;
+                    mq_push(&S.mq, (fin_row << 8) | fin_kvh);
+                }
+            }
+            fin = false;
+        };
         for (uint32_t it = 0;; ++it) {
             mbar_wait(&S.mready[it % kMeta], (it / kMeta) & 1u);
             const TileMeta md = S.meta[it % kMeta];
-            if (md.item < 0) break;
+            if (md.item < 0) {
+                if (fin) finish();
+                break;
+            }
             if (md.flags & 1) {
 #pragma unroll
                 for (int h = 0; h < GI; ++h) {
@@ -482,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.p_full[ob]);
+            if (fin) finish();  // the previous item, now that P^T(it) is queued
             // ---- O^T of the PREVIOUS tile (deferred so this tile's softmax did
             //      not wait for its P.V round trip): acc = acc*corr_prev + O_prev
             if (pending) {
@@ -500,51 +558,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int h = 0; h < GI; ++h) corr_prev[h] = corr[h];
             pending = true;
             if (md.flags & 2) {
-                // ---- flush this tile's O^T, then finalize the item
-                mbar_wait(&S.o_full[ob], oph);
-                tc_fence_after();
-                float o[GI];
-                tmem_ld<GI>(tmem_o0 + ob * kN + lane_addr, o);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.o_free[ob]);
+                // last tile of the item: finish() accumulates its O^T and
+                // writes the record during the next tile
 #pragma unroll
-                for (int h = 0; h < GI; ++h) acc[h] = acc[h] * corr[h] + o[h];
+                for (int h = 0; h < GI; ++h) {
+                    fin_acc[h] = acc[h];
+                    fin_corr[h] = corr[h];
+                    fin_m[h] = m[h];
+                    fin_l[h] = l[h];
+                }
+                fin_ob = ob;
+                fin_oph = oph;
+                fin_rec0 = static_cast<int64_t>(md.gchunk) * p.num_q_heads + static_cast<int64_t>(md.kvh) * G;
+                fin_ntok = static_cast<float>(md.thi - md.tlo);
+                fin_row = md.row;
+                fin_kvh = md.kvh;
+                fin = true;
                 pending = false;
-                // e = sum over the 128 token rows of l
-#pragma unroll
-                for (int h = 0; h < GI; ++h) {
-                    float v = l[h];
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                    if (lane == 0) S.red_sum[ew][h] = v;
-                }
-                named_bar_sync(1, 128);
-                const int64_t rec0 = static_cast<int64_t>(md.gchunk) * p.num_q_heads +
-                                     static_cast<int64_t>(md.kvh) * G;
-#pragma unroll
-                for (int h = 0; h < GI; ++h) {
-                    if (h >= G) continue;
-                    float* rec = recs + (rec0 + h) * (kD + 4);
-                    rec[4 + row] = acc[h];
-                    if (row == 0) {
-                        rec[0] = m[h] * 0.6931471805599453f;
-                        rec[1] = (S.red_sum[0][h] + S.red_sum[1][h]) + (S.red_sum[2][h] + S.red_sum[3][h]);
-                        rec[2] = static_cast<float>(md.thi - md.tlo);
-                        rec[3] = 0.f;
-                    }
-                }
-                named_bar_sync(1, 128);
-                if (p.fused_mode != 0 && warp == 2 && lane == 0) {
-                    // group completion (see K1): the CTA that wrote the last
-                    // chunk of (row, kv head) hands it to the merge warp
-                    const int gi = md.row * p.num_kv_heads + md.kvh;
-                    const int old = atomic_add_acq_rel_gpu(p.group_counter + gi, 1);
-                    if (old + 1 == __ldg(p.group_expected + gi)) {
-                        p.group_counter[gi] = 0;
-                        mq_push(&S.mq, (md.row << 8) | md.kvh);
-                    }
-                }
             }
         }
         if (p.fused_mode != 0) {
