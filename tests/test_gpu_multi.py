@@ -1,5 +1,6 @@
-"""Multi-GPU parity of dattn_decode_sharded (one process per GPU, NCCL
-allgather of (m, e, ma) records between ranks). Needs >= 2 visible GPUs;
+"""Multi-GPU parity of dattn_decode_sharded (one process per GPU; the (m, e,
+ma) records cross GPUs through K5's NVLink exchange, the NCCL allgather
+alternative or the in-kernel push + K6). Needs >= 2 visible GPUs;
 skipped otherwise (the single-GPU round-end run cannot exercise it)."""
 import os
 import socket
@@ -32,6 +33,7 @@ MODES = {"k5_nvlink": {"DATTN_FUSED_MERGE": "1"}, "nccl": {"DATTN_FUSED_MERGE": 
 CASES = {
     "gqa_bf16": dict(lens=[5000, 37, 20000, 1, 16], hq=64, hkv=8, d=128, dtype=0, tol=2e-2),
     "mha_f32": dict(lens=[4096, 3, 777], hq=32, hkv=32, d=128, dtype=1, tol=1e-3),
+    "mha_f64": dict(lens=[900, 5, 2000], hq=8, hkv=8, d=64, dtype=2, tol=1e-10),
 }
 
 
@@ -69,7 +71,7 @@ def _worker(rank, world, port, case, placement, fused, q):
             s = st.seq_create(rr.tokens)
             st.fill_synthetic(s, seed, rr.request, rr.tok_begin, 1.0, 2.0)
             ranges.append(pb.Range(s, rr.request, 0, rr.tokens))
-        tdt = {0: torch.bfloat16, 1: torch.float32}[dt]
+        tdt = {0: torch.bfloat16, 1: torch.float32, 2: torch.float64}[dt]
         qd = torch.empty(len(lens), hq, st.padded_dim, dtype=tdt, device=f"cuda:{rank}")
         st.q_fill_synthetic(qd, len(lens), seed)
         out = torch.zeros_like(qd)
@@ -85,6 +87,26 @@ def _worker(rank, world, port, case, placement, fused, q):
         for _ in range(20):
             st.decode_sharded(ranges, len(lens), qd, out)
         torch.cuda.synchronize()
+        # steps whose inputs change: two query sets and a batch in which rank 0
+        # holds no tokens of request 0 (identity record), interleaved; every
+        # step must reproduce its first result bit for bit (a stale or
+        # half-arrived exchange record would not)
+        qd2 = torch.empty_like(qd)
+        st.q_fill_synthetic(qd2, len(lens), seed + 1)
+        ranges_c = [pb.Range(r.seq, r.out_row, 0, 0) if (rank == 0 and r.out_row == 0) else r for r in ranges]
+        variants = [(ranges, qd), (ranges, qd2), (ranges_c, qd)]
+        firsts = []
+        for rg, qq in variants:
+            o = torch.zeros_like(qd)
+            st.decode_sharded(rg, len(lens), qq, o)
+            firsts.append(o)
+        stable = bool(torch.equal(firsts[0], out))
+        for k in range(12):
+            rg, qq = variants[k % 3]
+            o = torch.zeros_like(qd)
+            st.decode_sharded(rg, len(lens), qq, o)
+            torch.cuda.synchronize()
+            stable &= bool(torch.equal(o, firsts[k % 3]))
         # host-memory path gives the same bytes
         qh = qd.cpu().pin_memory()
         oh = torch.zeros_like(qh).pin_memory()
@@ -100,7 +122,7 @@ def _worker(rank, world, port, case, placement, fused, q):
         allg = [torch.zeros_like(g) for _ in range(world)]
         dist.all_gather(allg, g)
         agree = all(torch.equal(allg[0], x) for x in allg)
-        q.put((rank, err, agree, same, None))
+        q.put((rank, err, agree, same and stable, None))
         dist.destroy_process_group()
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, None, False, False, repr(e)))
