@@ -82,14 +82,10 @@ int elem_bytes_for(int dtype) { return dtype == kBF16 ? 2 : (dtype == kF32 ? 4 :
 void dattn_store::release_exchange() {
     for (int r = 0; r < 8; ++r) {
         if (r != rank && peer_x[r]) cudaIpcCloseMemHandle(peer_x[r]);
-        if (r != rank && peer_flags[r]) cudaIpcCloseMemHandle(peer_flags[r]);
         peer_x[r] = nullptr;
-        peer_flags[r] = nullptr;
     }
     if (xbuf) cudaFree(xbuf);
-    if (xflags) cudaFree(xflags);
     xbuf = nullptr;
-    xflags = nullptr;
     fused_merge = false;
 }
 
@@ -101,57 +97,39 @@ void dattn_store::setup_exchange() {
     if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
     slot_stride = static_cast<int64_t>(cfg.max_seqs) * cfg.num_q_heads;
     // two halves, used by alternate steps (epoch parity): a rank that runs one
-    // step ahead never overwrites records or flags a slower peer still reads
+    // step ahead never writes into the half a slower peer still reads
     xhalf = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
     const size_t xbytes = 2 * xhalf;
-    flag_stride = std::max<int64_t>(kMaxExchangeGrid, static_cast<int64_t>(cfg.max_seqs) * cfg.num_kv_heads);
-    fhalf = static_cast<size_t>(nranks) * flag_stride;
-    // flags (two halves), then the monotonic per-source group counters (uint64)
-    const size_t fbytes = 2 * fhalf * sizeof(uint32_t) + (static_cast<size_t>(nranks) + 2) * sizeof(uint64_t);
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&xflags), fbytes), "cudaMalloc(flags)");
-    cuda_check(cudaMemsetAsync(xflags, 0, fbytes, stream), "cudaMemset(flags)");
     // every exchange word starts empty (all ones, see XWord in dattn_merge.cuh)
     cuda_check(cudaMemsetAsync(xbuf, 0xFF, xbytes, stream), "cudaMemset(exchange)");
-    cudaIpcMemHandle_t hx, hf;
+    cudaIpcMemHandle_t hx;
     cuda_check(cudaIpcGetMemHandle(&hx, xbuf), "cudaIpcGetMemHandle");
-    cuda_check(cudaIpcGetMemHandle(&hf, xflags), "cudaIpcGetMemHandle");
     constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-    std::vector<unsigned char> mine(2 * kH), all(2 * kH * nranks);
-    std::memcpy(mine.data(), &hx, kH);
-    std::memcpy(mine.data() + kH, &hf, kH);
+    std::vector<unsigned char> all(kH * nranks);
     DevBuf dh;
     dh.ensure(all.size());
-    cuda_check(cudaMemcpyAsync(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, mine.data(), 2 * kH,
-                               cudaMemcpyHostToDevice, stream),
+    cuda_check(cudaMemcpyAsync(static_cast<unsigned char*>(dh.p) + rank * kH, &hx, kH, cudaMemcpyHostToDevice,
+                               stream),
                "cudaMemcpyAsync");
-    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, dh.p, 2 * kH, ncclUint8,
-                             comm, stream),
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, stream),
                "ncclAllGather(ipc handles)");
-    cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream),
-               "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     for (int r = 0; r < nranks; ++r) {
         if (r == rank) {
             peer_x[r] = xbuf;
-            peer_flags[r] = xflags;
             continue;
         }
-        cudaIpcMemHandle_t px, pf;
-        std::memcpy(&px, all.data() + r * 2 * kH, kH);
-        std::memcpy(&pf, all.data() + r * 2 * kH + kH, kH);
+        cudaIpcMemHandle_t px;
+        std::memcpy(&px, all.data() + r * kH, kH);
         cuda_check(cudaIpcOpenMemHandle(&peer_x[r], px, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-        void* f = nullptr;
-        cuda_check(cudaIpcOpenMemHandle(&f, pf, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-        peer_flags[r] = static_cast<uint32_t*>(f);
     }
-    // every rank has emptied its exchange buffer and zeroed its flags before anyone can publish
-    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * 2 * kH, dh.p, 2 * kH, ncclUint8,
-                             comm, stream),
+    // every rank has emptied its exchange buffer before anyone can push
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, stream),
                "ncclAllGather(barrier)");
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     epoch = 0;
-    count_target = 0;
     fused_merge = true;
 }
 
@@ -375,7 +353,10 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
         int64_t c = std::max<int64_t>(work / std::max<int64_t>(target, 1), 1);
         int64_t p2 = 1;
         while (p2 * 2 <= c) p2 *= 2;
-        const int64_t lo = tc_ok ? 128 : std::max<int64_t>(ma_stage_tokens(cfg.dtype, dp), 64);
+        // floor 512 tokens: below it the per-item cost outweighs the extra
+        // parallelism (config 1, 4K fp32 tokens x 32 heads: 64-token chunks
+        // 36.7 us per step, 512-token chunks 29.6 us)
+        const int64_t lo = std::max<int64_t>(512, tc_ok ? 128 : ma_stage_tokens(cfg.dtype, dp));
         C = std::min<int64_t>(std::max<int64_t>(p2, lo), 8192);
         if (C % cfg.page_tokens) C = (C / cfg.page_tokens + 1) * cfg.page_tokens;
     }
@@ -721,17 +702,11 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         MAParams f{};
         fill_fused(pl, f);
         f.fused_mode = 2;
-        f.epoch = ++epoch;
-        for (int r = 0; r < nranks; ++r) {
-            f.peer_x[r] = xhalf_ptr(peer_x[r], f.epoch);
-            f.peer_flags[r] = fhalf_ptr(peer_flags[r], f.epoch);
-        }
+        ++epoch;
+        for (int r = 0; r < nranks; ++r) f.peer_x[r] = xhalf_ptr(peer_x[r], epoch);
         f.rank = rank;
         f.nranks = nranks;
         f.slot_stride = slot_stride;
-        f.flag_stride = flag_stride;
-        for (int r = 0; r < nranks; ++r) f.peer_count[r] = counters_of(peer_flags[r]);
-        count_target += static_cast<unsigned long long>(b.num_rows) * cfg.num_kv_heads;
         run_ma(pl, q_dev, recs.p, b.scale, false, &f);
         RankMergeParams rp{};
         rp.rows = b.num_rows;
@@ -739,18 +714,11 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         rp.group = group;
         rp.num_kv_heads = cfg.num_kv_heads;
         rp.group_expected = static_cast<const int32_t*>(d_meta.p) + pl.off_expect;
-        for (int r = 0; r < nranks; ++r) {
-            rp.peer_x[r] = f.peer_x[r];
-            rp.peer_flags[r] = f.peer_flags[r];
-        }
+        for (int r = 0; r < nranks; ++r) rp.peer_x[r] = f.peer_x[r];
         rp.rank = rank;
         rp.nranks = nranks;
         rp.slot_stride = slot_stride;
-        rp.flag_stride = flag_stride;
-        rp.epoch = f.epoch;
         rp.out_norm = out_dev0;
-        for (int r = 0; r < nranks; ++r) rp.peer_count[r] = f.peer_count[r];
-        rp.count_target = count_target;
         // all CTAs co-resident (<= 4 per SM): identity pushes precede every wait
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8, static_cast<int64_t>(num_sms) * 4)));
@@ -780,15 +748,11 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.local.c_stride = cfg.num_q_heads;
         xp.local.chunk_kvh = pl.any_kvh ? w + pl.off_kvh : nullptr;
         xp.local.group = group;
-        xp.epoch = ++epoch;
-        for (int r = 0; r < nranks; ++r) {
-            xp.peer_x[r] = xhalf_ptr(peer_x[r], xp.epoch);
-            xp.peer_flags[r] = fhalf_ptr(peer_flags[r], xp.epoch);
-        }
+        ++epoch;
+        for (int r = 0; r < nranks; ++r) xp.peer_x[r] = xhalf_ptr(peer_x[r], epoch);
         xp.rank = rank;
         xp.nranks = nranks;
         xp.slot_stride = slot_stride;
-        xp.flag_stride = flag_stride;
         xp.out_norm = out_dev0;
         // 8 warps per group for long chunk lists, else one; the grid depends
         // only on the row count and chunk shape, identical on every rank, and

@@ -92,25 +92,15 @@ struct dattn_store {
 
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
-    // K5 exchange: IPC-mapped record/flag buffers of every rank
-    void* xbuf = nullptr;        // own [nranks][slot_stride][rec]
-    uint32_t* xflags = nullptr;  // own [nranks][slot_stride]
+    // exchange buffers (K5 / K6): IPC-mapped, two halves used by alternate steps
+    void* xbuf = nullptr;  // own [2][nranks][slot_stride][rec]
     void* peer_x[8]{};
-    uint32_t* peer_flags[8]{};
     int64_t slot_stride = 0;
-    int64_t flag_stride = 0;
-    size_t xhalf = 0, fhalf = 0;  // bytes / flags of one exchange half
+    size_t xhalf = 0;  // bytes of one exchange half
     void* xhalf_ptr(void* base, uint32_t ep) const {
         return static_cast<unsigned char*>(base) + (ep & 1u) * xhalf;
     }
-    uint32_t* fhalf_ptr(uint32_t* base, uint32_t ep) const { return base + (ep & 1u) * fhalf; }
-    // per-source delivered-group counters behind the two flag halves (8-B aligned)
-    unsigned long long* counters_of(uint32_t* flags_base) const {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(flags_base + 2 * fhalf);
-        return reinterpret_cast<unsigned long long*>((a + 7) & ~uintptr_t(7));
-    }
-    unsigned long long count_target = 0;
-    uint32_t epoch = 0;
+    uint32_t epoch = 0;  // step counter: its parity selects the half
     bool fused_merge = false;
     void setup_exchange();
     void release_exchange();

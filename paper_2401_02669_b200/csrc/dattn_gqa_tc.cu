@@ -324,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 7) {
         // ================================ merge warp (fused modes)
         if (p.fused_mode != 0) {
-            unsigned int pushed = 0;
             for (int idx = 0;; ++idx) {
                 int32_t v = 0;
                 if (lane == 0) v = mq_pop(&S.mq, idx);
@@ -332,11 +331,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (v < 0) break;
                 __threadfence();
                 warp_group_merge<bf16_t, kD, (GI < 8 ? GI : 8)>(p, v >> 8, v & 0xFF, lane);
-                ++pushed;
-            }
-            if (p.fused_mode == 2) {
-                __syncwarp();
-                if (lane == 0) publish_pushed(p, pushed);
             }
         }
     } else if (warp == 6) {

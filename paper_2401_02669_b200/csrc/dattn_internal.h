@@ -51,14 +51,10 @@ struct MAParams {
     const int32_t* chunk_kvh;        // per chunk kv-head tag (-1 all) or null
     void* out_norm;                  // [rows][Hq][DP] storage dtype
     void* out_recs;                  // [rows][Hq][DP+4] or null
-    void* peer_x[8];
-    uint32_t* peer_flags[8];
+    void* peer_x[8];                 // this step's exchange half of every rank
     int32_t rank;
     int32_t nranks;
     int64_t slot_stride;             // records per source rank
-    int64_t flag_stride;             // flags per source rank
-    uint32_t epoch;
-    unsigned long long* peer_count[8];  // per destination: [nranks] groups received per source
 };
 
 // K6: rank merge after fused K1/K2 (waits until every rank delivered all groups).
@@ -69,15 +65,10 @@ struct RankMergeParams {
     int32_t num_kv_heads;
     const int32_t* group_expected;   // this rank's [rows][Hkv]: 0 -> push identity
     void* peer_x[8];
-    uint32_t* peer_flags[8];
     int32_t rank;
     int32_t nranks;
     int64_t slot_stride;
-    int64_t flag_stride;
-    uint32_t epoch;
     void* out_norm;
-    unsigned long long* peer_count[8];
-    unsigned long long count_target;  // cumulative groups per source after this step
 };
 
 // K3 merge launch.
@@ -97,16 +88,13 @@ struct MergeParams {
 
 // K5: fused local merge + NVLink exchange + rank merge (one launch per step).
 constexpr int kMaxRanks = 8;
-constexpr int kMaxExchangeGrid = 1024;  // K5 CTAs (flags per source rank)
+constexpr int kMaxExchangeGrid = 1024;  // K5 CTAs
 struct XParams {
     MergeParams local;                 // chunk records of this rank (out_* unused)
-    void* peer_x[kMaxRanks];           // exchange buffers of every rank (own at [rank])
-    uint32_t* peer_flags[kMaxRanks];   // arrival flags of every rank
+    void* peer_x[kMaxRanks];           // this step's exchange half of every rank (own at [rank])
     int32_t rank;
     int32_t nranks;
     int64_t slot_stride;               // records per source rank in an exchange buffer
-    int64_t flag_stride;               // flags per source rank (>= grid)
-    uint32_t epoch;                    // this step's flag value
     int32_t warps_per_group;           // 1 or 8 (long chunk lists); local choice
     int32_t groups_per_cta;            // 8 or 1; identical on every rank
     void* out_norm;                    // [rows*heads][DP] storage dtype

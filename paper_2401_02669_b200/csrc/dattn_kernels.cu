@@ -163,7 +163,6 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
         // merges each (row, kv head) group whose last chunk this CTA wrote,
         // concurrently with the streaming warps
         if (p.fused_mode == 0) return;
-        unsigned int pushed = 0;
         for (int idx = 0;; ++idx) {
             int32_t v = 0;
             if (lane == 0) v = mq_pop(&mq, idx);
@@ -171,11 +170,6 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             if (v < 0) break;
             __threadfence();  // acquire the other CTAs' records of the group
             warp_group_merge<T, DP, (sizeof(T) == 8 ? 2 : 8)>(p, v >> 8, v & 0xFF, lane);
-            ++pushed;
-        }
-        if (p.fused_mode == 2) {
-            __syncwarp();
-            if (lane == 0) publish_pushed(p, pushed);
         }
         return;
     }
@@ -839,183 +833,47 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     }
     stamp(1);
 
-    // ---- D. rank merge, one warp per group: lane r reads rank r's header,
-    //      every lane its payload words of each live record, in rank order
+    // ---- D. rank merge, one warp per group (xchg_rank_merge)
     U* X = static_cast<U*>(x.peer_x[x.rank]);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
-         g += static_cast<int64_t>(gridDim.x) * kMergeWarps) {
-        Acc mr = kNegInf, er = 0, tr = 0;
-        if (lane < x.nranks) {
-            U h[4];
-            x_poll<U, 4>(X + (static_cast<int64_t>(lane) * x.slot_stride + g) * REC, h);
-            mr = x_dec<Acc>(h[0]);
-            er = x_dec<Acc>(h[1]);
-            tr = x_dec<Acc>(h[2]);
-        }
-        Acc m2 = tr != Acc(0) ? mr : kNegInf;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, off));
-        const Acc wl = tr != Acc(0) ? ((mr == m2) ? Acc(1) : exp(mr - m2)) : Acc(0);
-        Acc e2 = 0, tok2 = 0;
-        Acc a2[kSweeps][kVW];
-#pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw)
-#pragma unroll
-            for (int v = 0; v < kVW; ++v) a2[sw][v] = 0;
-        unsigned live_mask = 0;
-        for (int r = 0; r < x.nranks; ++r) {
-            const Acc tk = __shfl_sync(0xffffffffu, tr, r);
-            const Acc w = __shfl_sync(0xffffffffu, wl, r);
-            const Acc er_r = __shfl_sync(0xffffffffu, er, r);
-            if (tk == Acc(0)) continue;  // warp-uniform
-            live_mask |= 1u << r;
-            e2 += er_r * w;
-            tok2 += tk;
-            const U* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-#pragma unroll
-            for (int sw = 0; sw < kSweeps; ++sw) {
-                const int j = sw * kPer + lane * kVW;
-                if (j < DP) {
-                    U d[kVW];
-                    x_poll<U, kVW>(rec + 4 + j, d);
-#pragma unroll
-                    for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(d[v]) * w;
-                }
-            }
-        }
-        __syncwarp();
-        // empty the slots for the step after next
-        for (int r = 0; r < x.nranks; ++r) {
-            U* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            if (lane == r) x_clear<U, 4>(rec);
-            if (live_mask & (1u << r)) {
-#pragma unroll
-                for (int sw = 0; sw < kSweeps; ++sw) {
-                    const int j = sw * kPer + lane * kVW;
-                    if (j < DP) x_clear<U, kVW>(rec + 4 + j);
-                }
-            }
-        }
-        T* o = static_cast<T*>(x.out_norm) + g * DP;
-#pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw) {
-            const int j = sw * kPer + lane * kVW;
-            if (j < DP)
-#pragma unroll
-                for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(tok2 != Acc(0) ? a2[sw][v] / e2 : Acc(0));
-        }
-    }
+         g += static_cast<int64_t>(gridDim.x) * kMergeWarps)
+        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane);
     __syncthreads();
     stamp(4);
 }
 
 // ------------------------------------------------------------------ K6
-// Rank merge after the fused K1/K2: one warp per (row, q head). This rank
-// first publishes identity records for its groups that hold no tokens (no MA
-// CTA completes them), then every CTA waits until each rank's delivered-group
-// counter reaches this step's cumulative target and merges the nranks records
-// into the output. CTAs never wait for each other on this GPU; the counters
-// are advanced by the peers' MA kernels (per CTA, at exit) and K6s.
+// Rank merge after the in-kernel merge + push of K1/K2 (fused mode 2): this
+// rank first pushes identity headers for its (row, kv head) groups that hold
+// no tokens (no MA CTA completes them), then one warp per (row, q head) merges
+// the nranks records as they arrive (xchg_rank_merge: self-validating words,
+// no counters or fences).
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const RankMergeParams x) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
+    using U = typename XWord<Acc>::U;
     constexpr int REC = DP + 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t ngroups_kv = static_cast<int64_t>(x.rows) * x.num_kv_heads;
-    unsigned int mine = 0;
-    // identity records for empty (row, kv head) groups of this rank
+    const U hdr[4] = {x_enc(kNegInf), x_enc(Acc(0)), x_enc(Acc(0)), x_enc(Acc(0))};
     for (int64_t gk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gk < ngroups_kv;
          gk += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (x.group_expected[gk] != 0) continue;
         const int row = static_cast<int>(gk / x.num_kv_heads), kvh = static_cast<int>(gk % x.num_kv_heads);
         for (int hh = 0; hh < x.group; ++hh) {
             const int64_t g = static_cast<int64_t>(row) * x.heads + kvh * x.group + hh;
-            for (int r = 0; r < x.nranks; ++r) {
-                Acc* dst = static_cast<Acc*>(x.peer_x[r]) + (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC;
-                dst[0] = kNegInf;
-                dst[1] = 0;
-                dst[2] = 0;
-                dst[3] = 0;  // ma is never read for identity records
-            }
-        }
-        ++mine;
-    }
-    // publish this CTA's identity pushes (one system fence per CTA)
-    __shared__ unsigned int s_cnt;
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    if (mine) atomicAdd(&s_cnt, mine);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_cnt) {
-        __threadfence_system();
-        for (int r = 0; r < x.nranks; ++r)
-            atomicAdd_system(x.peer_count[r] + x.rank, static_cast<unsigned long long>(s_cnt));
-    }
-    // wait until every rank delivered all (row, kv head) groups of this step
-    if (threadIdx.x < x.nranks) {
-        const unsigned long long* c = x.peer_count[x.rank] + threadIdx.x;
-        uint64_t t0 = 0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned long long v;
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
-            if (v >= x.count_target) break;
-            __nanosleep(64);
-            uint64_t t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 10000000000ull) __trap();
+            for (int r = 0; r < x.nranks; ++r)
+                x_store<U, 4>(static_cast<U*>(x.peer_x[r]) + (static_cast<int64_t>(x.rank) * x.slot_stride + g) * REC,
+                              hdr);
         }
     }
-    __syncthreads();
     const int64_t groups = static_cast<int64_t>(x.rows) * x.heads;
-    const Acc* X = static_cast<const Acc*>(x.peer_x[x.rank]);
+    U* X = static_cast<U*>(x.peer_x[x.rank]);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
-         g += static_cast<int64_t>(gridDim.x) * kMergeWarps) {
-        const int row = static_cast<int>(g / x.heads);
-        const int h = static_cast<int>(g - static_cast<int64_t>(row) * x.heads);
-        const int64_t gk = static_cast<int64_t>(row) * x.num_kv_heads + h / x.group;
-        (void)gk;
-        Acc m2 = kNegInf;
-        for (int r = 0; r < x.nranks; ++r) {
-            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            if (__ldcv(rec + 2) != Acc(0)) m2 = fmax(m2, __ldcv(rec));
-        }
-        Acc e2 = 0, tok2 = 0;
-        constexpr int EPL = (DP + 31) / 32;
-        Acc a2[EPL];
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) a2[k] = 0;
-        for (int r = 0; r < x.nranks; ++r) {
-            const Acc* rec = X + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            const Acc tk = __ldcv(rec + 2);
-            if (tk == Acc(0)) continue;
-            const Acc mr = __ldcv(rec);
-            const Acc w = (mr == m2) ? Acc(1) : exp(mr - m2);
-            e2 += __ldcv(rec + 1) * w;
-            tok2 += tk;
-#pragma unroll
-            for (int k = 0; k < EPL; ++k) {
-                const int j = lane + 32 * k;
-                if (j < DP) a2[k] += __ldcv(rec + 4 + j) * w;
-            }
-        }
-        // empty the slots (the all-ones word K5 reads as "not arrived"): the
-        // delivered counters already proved every word landed
-        __syncwarp();
-        using U = typename XWord<Acc>::U;
-        for (int r = 0; r < x.nranks; ++r) {
-            U* rec = reinterpret_cast<U*>(const_cast<Acc*>(X)) + (static_cast<int64_t>(r) * x.slot_stride + g) * REC;
-            for (int j = lane; j < REC; j += 32) rec[j] = ~U(0);
-        }
-        T* o = static_cast<T*>(x.out_norm) + g * DP;
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) {
-            const int j = lane + 32 * k;
-            if (j < DP) o[j] = E::from_acc(tok2 != Acc(0) ? a2[k] / e2 : Acc(0));
-        }
-    }
+         g += static_cast<int64_t>(gridDim.x) * kMergeWarps)
+        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane);
 }
 
 // ------------------------------------------------------------------ K4

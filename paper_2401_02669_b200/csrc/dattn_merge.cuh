@@ -100,13 +100,29 @@ __device__ __forceinline__ Acc x_dec(typename XWord<Acc>::U b) {
     return v;
 }
 
-// N words at p (16-byte aligned when N*sizeof(U) is a multiple of 16)
+// N words at p (16-byte aligned when N*sizeof(U) is a multiple of 16); the
+// words are repacked into uint4 values so the arrays stay in registers
+template <class U>
+__device__ __forceinline__ uint4 x_pack(const U* w) {
+    if constexpr (sizeof(U) == 4) return make_uint4(w[0], w[1], w[2], w[3]);
+    else
+        return make_uint4(static_cast<uint32_t>(w[0]), static_cast<uint32_t>(w[0] >> 32),
+                          static_cast<uint32_t>(w[1]), static_cast<uint32_t>(w[1] >> 32));
+}
+template <class U>
+__device__ __forceinline__ void x_unpack(uint4 v, U* w) {
+    if constexpr (sizeof(U) == 4) {
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+        w[0] = (static_cast<U>(v.y) << 32) | v.x;
+        w[1] = (static_cast<U>(v.w) << 32) | v.z;
+    }
+}
 template <class U, int N>
 __device__ __forceinline__ void x_store(U* p, const U (&w)[N]) {
     if constexpr ((N * sizeof(U)) % 16 == 0) {
 #pragma unroll
-        for (int i = 0; i < N; i += 16 / sizeof(U))
-            *reinterpret_cast<uint4*>(p + i) = *reinterpret_cast<const uint4*>(&w[i]);
+        for (int i = 0; i < N; i += 16 / sizeof(U)) *reinterpret_cast<uint4*>(p + i) = x_pack<U>(w + i);
     } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) p[i] = w[i];
@@ -134,10 +150,7 @@ __device__ __forceinline__ void x_poll(const U* p, U (&w)[N]) {
         bool ok = true;
         if constexpr ((N * sizeof(U)) % 16 == 0) {
 #pragma unroll
-            for (int i = 0; i < N; i += 16 / sizeof(U)) {
-                const uint4 v = ld_volatile_v4(p + i);
-                *reinterpret_cast<uint4*>(&w[i]) = v;
-            }
+            for (int i = 0; i < N; i += 16 / sizeof(U)) x_unpack<U>(ld_volatile_v4(p + i), w + i);
         } else {
 #pragma unroll
             for (int i = 0; i < N; ++i) w[i] = *reinterpret_cast<const volatile U*>(p + i);
@@ -154,14 +167,6 @@ __device__ __forceinline__ void x_poll(const U* p, U (&w)[N]) {
     }
 }
 
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Warp-only group merge (the MA kernels' dedicated merge warp): for every q
 // head of kv head `kvh`, rescale-sum the row's chunk records and write the
@@ -288,11 +293,28 @@ __device__ void warp_group_merge(const MAParams& p, int row, int kvh, int lane) 
                             o[j + v] = E::from_acc(ntok != Acc(0) ? acc[hh][sw][v] / eg : Acc(0));
                 }
             }
-            const int nd = p.fused_mode == 2 ? p.nranks : (p.out_recs ? 1 : 0);
-            for (int d = 0; d < nd; ++d) {
-                Acc* dst = p.fused_mode == 2
-                               ? static_cast<Acc*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC
-                               : static_cast<Acc*>(p.out_recs) + g * REC;
+            if (p.fused_mode == 2) {
+                // every rank's exchange slot, in self-validating words (XWord)
+                using U = typename XWord<Acc>::U;
+                const U hdr[4] = {x_enc(ntok != Acc(0) ? mg[hh] : kNegInf), x_enc(eg), x_enc(ntok), x_enc(Acc(0))};
+                for (int d = 0; d < p.nranks; ++d) {
+                    U* dst = static_cast<U*>(p.peer_x[d]) + (static_cast<int64_t>(p.rank) * p.slot_stride + g) * REC;
+                    if (ntok != Acc(0)) {
+#pragma unroll
+                        for (int sw = 0; sw < kSweeps; ++sw) {
+                            const int j = sw * kPer + lane * kVW;
+                            if (j < DP) {
+                                U w[kVW];
+#pragma unroll
+                                for (int v = 0; v < kVW; ++v) w[v] = x_enc(acc[hh][sw][v]);
+                                x_store<U, kVW>(dst + 4 + j, w);
+                            }
+                        }
+                    }
+                    if (lane == 0) x_store<U, 4>(dst, hdr);
+                }
+            } else if (p.out_recs) {
+                Acc* dst = static_cast<Acc*>(p.out_recs) + g * REC;
 #pragma unroll
                 for (int sw = 0; sw < kSweeps; ++sw) {
                     const int j = sw * kPer + lane * kVW;
@@ -347,13 +369,83 @@ __device__ __forceinline__ int32_t mq_pop(MergeQueue* q, int idx) {
     return v;
 }
 
-// End of an MA kernel in fused mode 2: publish how many groups this CTA pushed
-// (one system fence per CTA instead of one per group); K6 waits on the sums.
-__device__ __forceinline__ void publish_pushed(const MAParams& p, unsigned int pushed) {
-    if (p.fused_mode != 2 || pushed == 0) return;
-    __threadfence_system();
-    for (int r = 0; r < p.nranks; ++r) atomicAdd_system(p.peer_count[r] + p.rank, static_cast<unsigned long long>(pushed));
+// Rank merge over the exchange buffer X ([nranks][slot_stride] records of
+// self-validating words): one warp per (row, q head) group g. Lane r reads
+// rank r's header, every lane its payload words of each live record, merged
+// in rank order into out (storage dtype); then the slots are emptied for the
+// step after next (a peer writes this half again only after it has seen this
+// rank's next-step records). Identity records carry only a header.
+template <typename T, int DP>
+__device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>::Acc>::U* X, int64_t g, int nranks,
+                                                int64_t slot_stride, void* out_norm, int lane) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    using U = typename XWord<Acc>::U;
+    constexpr int REC = DP + 4;
+    constexpr int kVW = (sizeof(Acc) == 4) ? (DP % 128 == 0 ? 4 : (DP % 64 == 0 ? 2 : 1))
+                                           : (DP % 64 == 0 ? 2 : 1);
+    constexpr int kPer = 32 * kVW;
+    constexpr int kSweeps = (DP + kPer - 1) / kPer;
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    Acc mr = kNegInf, er = 0, tr = 0;
+    if (lane < nranks) {
+        U h[4];
+        x_poll<U, 4>(X + (static_cast<int64_t>(lane) * slot_stride + g) * REC, h);
+        mr = x_dec<Acc>(h[0]);
+        er = x_dec<Acc>(h[1]);
+        tr = x_dec<Acc>(h[2]);
+    }
+    Acc m2 = tr != Acc(0) ? mr : kNegInf;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, off));
+    const Acc wl = tr != Acc(0) ? ((mr == m2) ? Acc(1) : exp(mr - m2)) : Acc(0);
+    Acc e2 = 0, tok2 = 0;
+    Acc a2[kSweeps][kVW];
+#pragma unroll
+    for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+        for (int v = 0; v < kVW; ++v) a2[sw][v] = 0;
+    unsigned live_mask = 0;
+    for (int r = 0; r < nranks; ++r) {
+        const Acc tk = __shfl_sync(0xffffffffu, tr, r);
+        const Acc w = __shfl_sync(0xffffffffu, wl, r);
+        const Acc er_r = __shfl_sync(0xffffffffu, er, r);
+        if (tk == Acc(0)) continue;  // warp-uniform
+        live_mask |= 1u << r;
+        e2 += er_r * w;
+        tok2 += tk;
+        const U* rec = X + (static_cast<int64_t>(r) * slot_stride + g) * REC;
+#pragma unroll
+        for (int sw = 0; sw < kSweeps; ++sw) {
+            const int j = sw * kPer + lane * kVW;
+            if (j < DP) {
+                U dw[kVW];
+                x_poll<U, kVW>(rec + 4 + j, dw);
+#pragma unroll
+                for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(dw[v]) * w;
+            }
+        }
+    }
+    __syncwarp();
+    for (int r = 0; r < nranks; ++r) {
+        U* rec = X + (static_cast<int64_t>(r) * slot_stride + g) * REC;
+        if (lane == r) x_clear<U, 4>(rec);
+        if (live_mask & (1u << r)) {
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP) x_clear<U, kVW>(rec + 4 + j);
+            }
+        }
+    }
+    T* o = static_cast<T*>(out_norm) + g * DP;
+#pragma unroll
+    for (int sw = 0; sw < kSweeps; ++sw) {
+        const int j = sw * kPer + lane * kVW;
+        if (j < DP)
+#pragma unroll
+            for (int v = 0; v < kVW; ++v) o[j + v] = E::from_acc(tok2 != Acc(0) ? a2[sw][v] / e2 : Acc(0));
+    }
 }
-
 
 }  // namespace dattn
