@@ -134,17 +134,28 @@ void dattn_store::setup_exchange() {
 }
 
 dattn_store::~dattn_store() {
-    if (!k5_trace_log.empty()) {
-        // DATTN_K5_TRACE summary: mean over calls (first 3 skipped), us from the first CTA start
-        std::array<double, 6> m{};
-        size_t n = 0;
-        for (size_t i = 3; i < k5_trace_log.size(); ++i, ++n)
-            for (int j = 0; j < 6; ++j) m[j] += k5_trace_log[i][j];
-        if (n)
-            std::fprintf(stderr,
-                         "[K5 trace rank %d] calls %zu: start spread %.2f us, A done(max) %.2f, end(max) %.2f, "
-                         "last t0 %.0f ns\n",
-                         rank, n, m[0] / n, m[1] / n, m[4] / n, k5_trace_log.back()[5]);
+    if (k5_trace.p) {
+        // DATTN_K5_TRACE summary over all calls: per-CTA mean phase-A and total
+        // durations, then the mean and max over CTAs
+        std::vector<unsigned long long> t(static_cast<size_t>(kMaxExchangeGrid) * 3);
+        if (cudaMemcpy(t.data(), k5_trace.p, t.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            double a_sum = 0, a_max = 0, e_sum = 0, e_max = 0;
+            int n = 0;
+            for (int c = 0; c < kMaxExchangeGrid; ++c) {
+                if (!t[c * 3 + 2]) continue;
+                const double a = 1e-3 * t[c * 3] / t[c * 3 + 2], e = 1e-3 * t[c * 3 + 1] / t[c * 3 + 2];
+                a_sum += a;
+                e_sum += e;
+                a_max = std::max(a_max, a);
+                e_max = std::max(e_max, e);
+                ++n;
+            }
+            if (n)
+                std::fprintf(stderr,
+                             "[K5 trace rank %d] %d CTAs x %llu calls: phase A mean %.2f max %.2f us; "
+                             "CTA total mean %.2f max %.2f us\n",
+                             rank, n, t[2], a_sum / n, a_max, e_sum / n, e_max);
+        }
     }
     release_exchange();
     if (comm) ncclCommDestroy(comm);
@@ -771,26 +782,17 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
                                  std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));
         static const bool trace = std::getenv("DATTN_K5_TRACE") != nullptr;
         if (trace) {
-            k5_trace.ensure(static_cast<size_t>(grid) * 5 * sizeof(unsigned long long));
+            if (!k5_trace.p) {
+                k5_trace.ensure(static_cast<size_t>(kMaxExchangeGrid) * 3 * sizeof(unsigned long long));
+                cuda_check(cudaMemsetAsync(k5_trace.p, 0, static_cast<size_t>(kMaxExchangeGrid) * 3 * 8, stream),
+                           "cudaMemsetAsync(trace)");
+            }
             xp.trace = static_cast<unsigned long long*>(k5_trace.p);
         }
         cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
         if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
         cuda_check(launch_merge_exchange(cfg.dtype, dp, xp, grid, stream), "launch(K5 merge_exchange)");
         if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
-        if (trace) {
-            std::vector<unsigned long long> t(static_cast<size_t>(grid) * 5);
-            cuda_check(cudaMemcpyAsync(t.data(), k5_trace.p, t.size() * 8, cudaMemcpyDeviceToHost, stream), "trace");
-            cuda_check(cudaStreamSynchronize(stream), "trace");
-            unsigned long long t0 = ~0ull, t0x = 0, mx[5] = {0, 0, 0, 0, 0};
-            for (int c = 0; c < grid; ++c) {
-                t0 = std::min(t0, t[c * 5]);
-                t0x = std::max(t0x, t[c * 5]);
-                for (int j = 1; j < 5; ++j) mx[j] = std::max(mx[j], t[c * 5 + j]);
-            }
-            k5_trace_log.push_back({(t0x - t0) * 1e-3, (mx[1] - t0) * 1e-3, (mx[2] - t0) * 1e-3,
-                                    (mx[3] - t0) * 1e-3, (mx[4] - t0) * 1e-3, static_cast<double>(t0)});
-        }
         count_launch(1);
         stats.last_exchange = 2;
         if (mem == DATTN_MEM_HOST) {

@@ -140,7 +140,6 @@ struct dattn_store {
     void fill_fused(const dattn::Plan& pl, dattn::MAParams& f);
     dattn::DevBuf gcounter;
     dattn::DevBuf k5_trace;                   // DATTN_K5_TRACE debug stamps
-    std::vector<std::array<double, 6>> k5_trace_log;
     size_t gcounter_elems = 0;
     void run_merge(const dattn::MergeParams& mp);
     void local_merge(const dattn::Plan& pl, const void* recs, void* out_recs, void* out_norm);

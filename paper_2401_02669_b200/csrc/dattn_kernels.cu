@@ -681,11 +681,19 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     pdl_wait();  // launched early behind the MA grid (PDL)
     const Acc* R = static_cast<const Acc*>(p.recs);
+    // DATTN_K5_TRACE: per-CTA sums over calls of (phase A done - start) and
+    // (end - start), %globaltimer ns, and the call count
+    uint64_t t_start = 0;
     auto stamp = [&](int i) {
         if (x.trace && threadIdx.x == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            x.trace[blockIdx.x * 5 + i] = t;
+            if (i == 0) {
+                t_start = t;
+            } else {
+                atomicAdd(x.trace + blockIdx.x * 3 + (i == 1 ? 0 : 1), t - t_start);
+                if (i == 4) atomicAdd(x.trace + blockIdx.x * 3 + 2, 1ull);
+            }
         }
     };
     stamp(0);
