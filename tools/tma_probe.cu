@@ -9,6 +9,8 @@
 //   mode 0: two 2-D TMA boxes of 64 columns x 16 rows, 128-B swizzle (K2 today)
 //   mode 1: one 1-D bulk copy of 4 KB (K1's path)
 //   mode 2: one 2-D TMA box of 128 columns x 16 rows, no swizzle
+//   mode 3: two 2-D TMA boxes of 64 columns x 16 rows, 128-B swizzle, over a
+//           half-split pool [pages][heads][2][16][64] (each box 2 KB contiguous)
 // Prints GB/s per mode. Build: nvcc -O3 -std=c++17 -gencode
 // arch=compute_100a,code=sm_100a -o tools/tma_probe tools/tma_probe.cu -lcuda
 #include <cuda.h>
@@ -88,9 +90,15 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
                     } else if (mode == 1) {
                         bulk_g2s(S.k[s] + pg * 4096, kpool + off, 4096, &S.kfull[s], pol);
                         bulk_g2s(S.v[s] + pg * 4096, vpool + off, 4096, &S.vfull[s], pol);
-                    } else {
+                    } else if (mode == 2) {
                         tma2d(S.k[s] + pg * 4096, &mk, 0, row0, &S.kfull[s], pol);
                         tma2d(S.v[s] + pg * 4096, &mv, 0, row0, &S.vfull[s], pol);
+                    } else {
+                        const int h0 = ((page * kHeads + kvh) * 2) * kP;  // half 0 rows, half 1 follows
+                        tma2d(S.k[s] + pg * 2048, &mk, 0, h0, &S.kfull[s], pol);
+                        tma2d(S.k[s] + kStageBytes / 2 + pg * 2048, &mk, 0, h0 + kP, &S.kfull[s], pol);
+                        tma2d(S.v[s] + pg * 2048, &mv, 0, h0, &S.vfull[s], pol);
+                        tma2d(S.v[s] + kStageBytes / 2 + pg * 2048, &mv, 0, h0 + kP, &S.vfull[s], pol);
                     }
                 }
             }
@@ -120,13 +128,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
 }
 
 static void make_map(CUtensorMap* m, void* base, uint64_t rows, int mode) {
-    cuuint64_t dims[2] = {kD, rows};
-    cuuint64_t strides[1] = {kD * 2};
-    cuuint32_t box[2] = {mode == 0 ? 64u : 128u, kP};
+    const bool half = mode == 3;  // [rows*2][64] view of the half-split pool
+    cuuint64_t dims[2] = {half ? 64u : kD, half ? 2 * rows : rows};
+    cuuint64_t strides[1] = {half ? 128u : kD * 2};
+    cuuint32_t box[2] = {(mode == 0 || half) ? 64u : 128u, kP};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          mode == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          (mode == 0 || mode == 3) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) std::printf("tensor map mode %d: error %d\n", mode, static_cast<int>(r));
 }
@@ -148,9 +157,9 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[3] = {"2-D TMA, two 64-col boxes, SW128 (K2)", "1-D bulk copy of 4 KB (K1)",
-                            "2-D TMA, one 128-col box, no swizzle"};
-    for (int mode = 0; mode < 3; ++mode) {
+    const char* names[4] = {"2-D TMA, two 64-col boxes, SW128 (K2)", "1-D bulk copy of 4 KB (K1)",
+                            "2-D TMA, one 128-col box, no swizzle", "2-D TMA, 64-col boxes, half-split pool"};
+    for (int mode = 0; mode < 4; ++mode) {
         CUtensorMap mk, mv;
         make_map(&mk, k, pages * kHeads * kP, mode);
         make_map(&mv, v, pages * kHeads * kP, mode);
