@@ -258,6 +258,8 @@ void dattn_store::init(const dattn_store_config& c) {
         const uint64_t rows = static_cast<uint64_t>(c.num_pages) * c.num_kv_heads * c.page_tokens;
         cuda_check(make_tmap_rows128(tm_k, kpool, rows, c.page_tokens), "tensor map (K pool)");
         cuda_check(make_tmap_rows128(tm_v, vpool, rows, c.page_tokens), "tensor map (V pool)");
+        cuda_check(make_tmap_tiles(tm_k4, kpool, c.num_pages, c.num_kv_heads, c.page_tokens), "tensor map (K tiles)");
+        cuda_check(make_tmap_tiles(tm_v4, vpool, c.num_pages, c.num_kv_heads, c.page_tokens), "tensor map (V tiles)");
         cuda_check(gqa_tc_configure(), "cudaFuncSetAttribute(K2)");
         tc_ok = true;
     }
@@ -531,7 +533,7 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     cudaEvent_t* ev = timing ? timer_pair(0) : nullptr;
     if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
     if (use_tc)
-        cuda_check(launch_gqa_tc(tm_k, tm_v, tm_q, p, grid, stream), "launch(K2 tcgen05)");
+        cuda_check(launch_gqa_tc(tm_k, tm_v, tm_q, tm_k4, tm_v4, p, grid, stream), "launch(K2 tcgen05)");
     else
         cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");

@@ -107,7 +107,7 @@ struct dattn_store {
 
     // K2 (tcgen05) path for grouped-query bf16 stores
     bool tc_ok = false;
-    alignas(64) unsigned char tm_k[128]{}, tm_v[128]{}, tm_q[128]{};
+    alignas(64) unsigned char tm_k[128]{}, tm_v[128]{}, tm_q[128]{}, tm_k4[128]{}, tm_v4[128]{};
     const void* tm_q_ptr = nullptr;
     int tm_q_rows = -1;
 

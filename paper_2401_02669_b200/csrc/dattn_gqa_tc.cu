@@ -85,6 +85,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// 4-D box {64 d, page rows, 1 kv head, 128/P pages}: a whole 128-token tile
+// half when the tile's pages are consecutive in the pool
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)),
+        "l"(policy)
+        : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -192,7 +204,8 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[NC]) {
 template <int GI>
 __global__ void __launch_bounds__(kThreads, 1)
     gqa_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                  const __grid_constant__ CUtensorMap tm_q, const MAParams p) {
+                  const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k4,
+                  const __grid_constant__ CUtensorMap tm_v4, const MAParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // the swizzle pattern is tied to 1024-B address alignment
     Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -238,6 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_v);
         prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k4);
+        prefetch_tmap(&tm_v4);
     }
     fence_async_smem();
     tc_fence_before();
@@ -295,18 +310,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                     md.kvh = kvh;
                     md.gchunk = gchunk;
                     md.npages = npages;
-                    for (int pg = 0; pg < npages; ++pg) md.page[pg] = S.pid[pg0 - win + pg];
+                    bool run = npages * P == kTile;  // a full tile of consecutive pages
+                    for (int pg = 0; pg < npages; ++pg) {
+                        md.page[pg] = S.pid[pg0 - win + pg];
+                        run = run && md.page[pg] == md.page[0] + pg;
+                    }
+                    md.flags |= run ? 4 : 0;
                     mbar_arrive(&S.mready[t % kMeta]);
                     const int ks = t % kKStages;
                     mbar_wait(&S.kempty[ks], ((t / kKStages) & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&S.kfull[ks], static_cast<uint32_t>(npages * P * 128 * 2 + G * 128 * 2));
                     uint8_t* sk = S.kst[ks];
                     uint8_t* sq = sk + kKVBytes;
-                    for (int pg = 0; pg < npages; ++pg) {
-                        const int row0 = (md.page[pg] * p.num_kv_heads + kvh) * P;
-                        const int off = pg * P * 128;
-                        tma_load_2d(sk + off, &tm_k, 0, row0, &S.kfull[ks], pol);
-                        tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.kfull[ks], pol);
+                    if (run) {
+                        // one box per 64-column half instead of two per page
+                        tma_load_4d(sk, &tm_k4, 0, 0, kvh, md.page[0], &S.kfull[ks], pol);
+                        tma_load_4d(sk + kHalf, &tm_k4, 64, 0, kvh, md.page[0], &S.kfull[ks], pol);
+                    } else {
+                        for (int pg = 0; pg < npages; ++pg) {
+                            const int row0 = (md.page[pg] * p.num_kv_heads + kvh) * P;
+                            const int off = pg * P * 128;
+                            tma_load_2d(sk + off, &tm_k, 0, row0, &S.kfull[ks], pol);
+                            tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.kfull[ks], pol);
+                        }
                     }
                     tma_load_2d(sq, &tm_q, 0, qrow, &S.kfull[ks], 0);
                     tma_load_2d(sq + kN * 128, &tm_q, 64, qrow, &S.kfull[ks], 0);
@@ -345,15 +371,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int page[kMaxTilePages];
 #pragma unroll
                 for (int pg = 0; pg < kMaxTilePages; ++pg) page[pg] = md.page[pg];
+                const bool run = (md.flags & 4) != 0;
                 const int vs = t % kVStages;
                 mbar_wait(&S.vempty[vs], ((t / kVStages) & 1u) ^ 1u);
                 mbar_arrive_expect_tx(&S.vfull[vs], static_cast<uint32_t>(npages * P * 128 * 2));
                 uint8_t* sv = S.vst[vs];
-                for (int pg = 0; pg < npages; ++pg) {
-                    const int row0 = (page[pg] * p.num_kv_heads + kvh) * P;
-                    const int off = pg * P * 128;
-                    tma_load_2d(sv + off, &tm_v, 0, row0, &S.vfull[vs], pol);
-                    tma_load_2d(sv + kHalf + off, &tm_v, 64, row0, &S.vfull[vs], pol);
+                if (run) {
+                    tma_load_4d(sv, &tm_v4, 0, 0, kvh, page[0], &S.vfull[vs], pol);
+                    tma_load_4d(sv + kHalf, &tm_v4, 64, 0, kvh, page[0], &S.vfull[vs], pol);
+                } else {
+                    for (int pg = 0; pg < npages; ++pg) {
+                        const int row0 = (page[pg] * p.num_kv_heads + kvh) * P;
+                        const int off = pg * P * 128;
+                        tma_load_2d(sv + off, &tm_v, 0, row0, &S.vfull[vs], pol);
+                        tma_load_2d(sv + kHalf + off, &tm_v, 64, row0, &S.vfull[vs], pol);
+                    }
                 }
             }
         }
@@ -616,6 +648,24 @@ cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, ui
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 4-D bf16 view {128 d, P rows, Hkv, pages} of a pool with a {64, P, 1, 128/P}
+// box and the 128-B swizzle: one copy moves a 64-column half of a whole tile
+// of consecutive pages into the same shared-memory layout as 128/P 2-D boxes.
+cudaError_t make_tmap_tiles(void* map_out, const void* base, uint64_t pages, uint32_t kv_heads, uint32_t page_tokens) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    cuuint64_t dims[4] = {128, page_tokens, kv_heads, pages};
+    cuuint64_t strides[3] = {128 * 2, static_cast<cuuint64_t>(page_tokens) * 256,
+                             static_cast<cuuint64_t>(kv_heads) * page_tokens * 256};
+    cuuint32_t box[4] = {64, page_tokens, 1, tc::kTile / page_tokens};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 static const void* gqa_fn(int group) {
     if (group <= 2) return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<2>);
     if (group <= 4) return reinterpret_cast<const void*>(&tc::gqa_tc_kernel<4>);
@@ -632,13 +682,11 @@ cudaError_t gqa_tc_configure() {
     return cudaSuccess;
 }
 
-cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const MAParams& p,
-                          int grid, cudaStream_t st) {
-    const CUtensorMap* k = static_cast<const CUtensorMap*>(tm_k);
-    const CUtensorMap* v = static_cast<const CUtensorMap*>(tm_v);
-    const CUtensorMap* q = static_cast<const CUtensorMap*>(tm_q);
+cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const void* tm_k4,
+                          const void* tm_v4, const MAParams& p, int grid, cudaStream_t st) {
     MAParams pp = p;
-    void* args[] = {const_cast<CUtensorMap*>(k), const_cast<CUtensorMap*>(v), const_cast<CUtensorMap*>(q), &pp};
+    void* args[] = {const_cast<void*>(tm_k), const_cast<void*>(tm_v), const_cast<void*>(tm_q),
+                    const_cast<void*>(tm_k4), const_cast<void*>(tm_v4), &pp};
     return cudaLaunchKernel(gqa_fn(p.group), dim3(grid), dim3(tc::kThreads), args, gqa_tc_smem_bytes(), st);
 }
 

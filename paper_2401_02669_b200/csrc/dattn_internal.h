@@ -175,9 +175,11 @@ cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_
 // K2 (tcgen05 GQA path, dattn_gqa_tc.cu)
 size_t gqa_tc_smem_bytes();
 cudaError_t gqa_tc_configure();
+cudaError_t make_tmap_tiles(void* map_out, const void* base, uint64_t pages, uint32_t kv_heads,
+                            uint32_t page_tokens);
 cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, uint32_t box_rows);
-cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const MAParams& p,
-                          int grid, cudaStream_t st);
+cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const void* tm_k4,
+                          const void* tm_v4, const MAParams& p, int grid, cudaStream_t st);
 cudaError_t launch_identity_records(int dtype, int dp, void* recs, int64_t n, cudaStream_t st);
 
 }  // namespace dattn

@@ -439,3 +439,56 @@ def test_reference_acceptance_gates_1_to_3_on_b200_adapter():
     for g in ("ACCEPTANCE  1 attention-equivalence-randomized: PASS",
               "ACCEPTANCE  2 partial-merge-algebra: PASS", "ACCEPTANCE  3 partial-wire-size-constant: PASS"):
         assert g in r.stdout
+
+
+def test_full_size_config4_vs_oracle_and_partition_invariance(torch_cuda):
+    """BASELINE config 4 at full size: 1 request x 1,048,576 tokens, MHA 32x128,
+    bf16 (16 GiB of KV). The GPU output matches the fp64 oracle. Splitting the
+    request into 16 rBlocks with 1024-token chunks, or one rBlock with 8192-token
+    chunks, gives the same output to fp32 re-association (partition invariance,
+    SPEC.md:105; test_distattention.cpp:107-131)."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    L = 1 << 20
+    st, seqs, q = make(torch, [L], 32, 32, 128, pb.BF16, seed=44)
+    one = out_np(torch, decode(torch, st, [pb.Range(seqs[0], 0, 0, L)], 1, q), 128)
+    cuts = [L * i // 16 for i in range(17)]
+    split = out_np(torch, decode(torch, st, [pb.Range(seqs[0], 0, a, b) for a, b in zip(cuts, cuts[1:])], 1, q,
+                                 chunk=1024), 128)
+    big = out_np(torch, decode(torch, st, [pb.Range(seqs[0], 0, 0, L)], 1, q, chunk=8192), 128)
+    assert np.isfinite(one).all()
+    # fp32 re-association only; the outputs are stored in bf16, so one output
+    # ulp (2^-8 of the row maximum at most) is the resolution of the comparison
+    assert rel_errs(split, one) < 4e-3
+    assert rel_errs(big, one) < 4e-3
+    ref = oracle.decode_ranges(44, [0], [L], [0], 32, 32, 128, dtype=pb.BF16)
+    assert rel_errs(one, ref) < 2e-2
+    st.close()
+
+
+def test_full_size_config3_tcgen05_vs_cuda_cores(torch_cuda):
+    """BASELINE config 3 at full size (16 x 131,072 tokens, GQA 64 q / 8 kv,
+    8 GiB of KV): K2 (tcgen05) and K1 (CUDA cores) agree, and one request
+    matches the fp64 oracle."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    lens = [131072] * 16
+    st, seqs, q = make(torch, lens, 64, 8, 128, pb.BF16, seed=33)
+    rg = [pb.Range(s, b, 0, L) for b, (s, L) in enumerate(zip(seqs, lens))]
+    got = out_np(torch, decode(torch, st, rg, 16, q), 128)
+    assert st.stats().last_kernel == 2
+    st.close()
+    os.environ["DATTN_DISABLE_TC"] = "1"
+    try:
+        st1, seqs1, q1 = make(torch, lens, 64, 8, 128, pb.BF16, seed=33)
+    finally:
+        del os.environ["DATTN_DISABLE_TC"]
+    ref1 = out_np(torch, decode(torch, st1, [pb.Range(s, b, 0, L) for b, (s, L) in enumerate(zip(seqs1, lens))],
+                                16, q1), 128)
+    assert st1.stats().last_kernel == 1
+    st1.close()
+    assert rel_errs(got, ref1) < 1e-2
+    ref = oracle.decode_ranges(33, [0], [131072], [0], 64, 8, 128, dtype=pb.BF16)
+    assert rel_errs(got[:1], ref) < 2e-2

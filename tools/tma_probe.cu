@@ -11,6 +11,8 @@
 //   mode 2: one 2-D TMA box of 128 columns x 16 rows, no swizzle
 //   mode 3: two 2-D TMA boxes of 64 columns x 16 rows, 128-B swizzle, over a
 //           half-split pool [pages][heads][2][16][64] (each box 2 KB contiguous)
+//   mode 4: one 4-D TMA box per 64-column half per TILE (8 consecutive pages:
+//           box 64 cols x 16 rows x 1 head x 8 pages, 128-B swizzle)
 // Prints GB/s per mode. Build: nvcc -O3 -std=c++17 -gencode
 // arch=compute_100a,code=sm_100a -o tools/tma_probe tools/tma_probe.cu -lcuda
 #include <cuda.h>
@@ -34,6 +36,15 @@ struct Smem {
     uint8_t v[kStages][kStageBytes];
     uint64_t kfull[kStages], kempty[kStages], vfull[kStages], vempty[kStages];
 };
+
+__device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* bar,
+                                      uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* bar, uint64_t pol) {
     asm volatile(
@@ -78,6 +89,14 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
                 mbar_arrive_expect_tx(&S.kfull[s], kStageBytes);
                 mbar_wait(&S.vempty[s], ph);
                 mbar_arrive_expect_tx(&S.vfull[s], kStageBytes);
+                if (mode == 4) {
+                    const int page = page0 + tp;
+                    tma4d(S.k[s], &mk, 0, 0, kvh, page, &S.kfull[s], pol);
+                    tma4d(S.k[s] + kStageBytes / 2, &mk, 64, 0, kvh, page, &S.kfull[s], pol);
+                    tma4d(S.v[s], &mv, 0, 0, kvh, page, &S.vfull[s], pol);
+                    tma4d(S.v[s] + kStageBytes / 2, &mv, 64, 0, kvh, page, &S.vfull[s], pol);
+                    continue;
+                }
                 for (int pg = 0; pg < kTilePages; ++pg) {
                     const int page = page0 + tp + pg;
                     const int row0 = (page * kHeads + kvh) * kP;
@@ -128,6 +147,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
 }
 
 static void make_map(CUtensorMap* m, void* base, uint64_t rows, int mode) {
+    if (mode == 4) {
+        cuuint64_t dims[4] = {kD, kP, kHeads, rows / (kHeads * kP)};
+        cuuint64_t strides[3] = {kD * 2, kP * kD * 2, kHeads * kP * kD * 2};
+        cuuint32_t box[4] = {64, kP, 1, kTilePages};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) std::printf("tensor map mode %d: error %d\n", mode, static_cast<int>(r));
+        return;
+    }
     const bool half = mode == 3;  // [rows*2][64] view of the half-split pool
     cuuint64_t dims[2] = {half ? 64u : kD, half ? 2 * rows : rows};
     cuuint64_t strides[1] = {half ? 128u : kD * 2};
@@ -157,9 +187,10 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const char* names[4] = {"2-D TMA, two 64-col boxes, SW128 (K2)", "1-D bulk copy of 4 KB (K1)",
-                            "2-D TMA, one 128-col box, no swizzle", "2-D TMA, 64-col boxes, half-split pool"};
-    for (int mode = 0; mode < 4; ++mode) {
+    const char* names[5] = {"2-D TMA, two 64-col boxes, SW128 (K2)", "1-D bulk copy of 4 KB (K1)",
+                            "2-D TMA, one 128-col box, no swizzle", "2-D TMA, 64-col boxes, half-split pool",
+                            "4-D TMA, one box per half per 8-page tile"};
+    for (int mode = 0; mode < 5; ++mode) {
         CUtensorMap mk, mv;
         make_map(&mk, k, pages * kHeads * kP, mode);
         make_map(&mv, v, pages * kHeads * kP, mode);
