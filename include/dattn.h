@@ -98,8 +98,12 @@ void dattn_store_destroy(dattn_store* s);
 dattn_status dattn_store_get_info(const dattn_store* s, dattn_store_info* out);
 /* The store's CUDA stream (cudaStream_t as void*). */
 dattn_status dattn_store_stream(const dattn_store* s, void** stream_out);
-/* Use a caller-owned stream (cudaStream_t) for all subsequent work; NULL
- * restores the store's own stream. */
+/* Use a caller-owned stream (cudaStream_t) for all subsequent work. NULL is
+ * the CUDA default stream, as everywhere in CUDA (e.g. torch's default stream
+ * handle 0), so store work is ordered with the caller's default-stream work;
+ * DATTN_OWN_STREAM restores the store's own non-blocking stream (the initial
+ * setting). */
+#define DATTN_OWN_STREAM ((void*)(intptr_t)-1)
 dattn_status dattn_store_set_stream(dattn_store* s, void* stream);
 dattn_status dattn_store_synchronize(dattn_store* s);
 

@@ -263,6 +263,9 @@ def _batch(ranges, num_rows: int, chunk_tokens: int, flags: int, scale: float):
     return b, arr
 
 
+OWN_STREAM = ctypes.c_void_p(-1).value  # DATTN_OWN_STREAM
+
+
 class Store:
     """Paged bf16/fp32/fp64 KV block store on one GPU (dattn_store)."""
 
@@ -319,6 +322,9 @@ class Store:
         return s.value or 0
 
     def set_stream(self, stream_ptr: Optional[int]):
+        """cudaStream_t handle for all later work. 0 / None is the CUDA default
+        stream (torch's default-stream handle); OWN_STREAM restores the store's
+        own non-blocking stream."""
         check(lib.dattn_store_set_stream(self._h, stream_ptr))
 
     def synchronize(self):

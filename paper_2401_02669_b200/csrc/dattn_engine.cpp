@@ -941,7 +941,9 @@ dattn_status dattn_store_set_stream(dattn_store* s, void* stream) {
         s->activate();
         // order the switch after all work already queued on the old stream
         cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
-        s->stream = stream ? static_cast<cudaStream_t>(stream) : s->own_stream;
+        // NULL is the CUDA default stream (not "unset"): a caller passing its
+        // default-stream handle gets ordering with its own default-stream work
+        s->stream = stream == DATTN_OWN_STREAM ? s->own_stream : static_cast<cudaStream_t>(stream);
     });
 }
 

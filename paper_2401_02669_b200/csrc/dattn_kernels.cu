@@ -20,6 +20,7 @@
 // batches balance across the 148 SMs.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -1128,8 +1129,9 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStre
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = std::getenv("DATTN_NO_PDL") != nullptr;  // debug switch
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = off ? 0 : 1;
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 

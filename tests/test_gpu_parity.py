@@ -492,3 +492,22 @@ def test_full_size_config3_tcgen05_vs_cuda_cores(torch_cuda):
     assert rel_errs(got, ref1) < 1e-2
     ref = oracle.decode_ranges(33, [0], [131072], [0], 64, 8, 128, dtype=pb.BF16)
     assert rel_errs(got[:1], ref) < 2e-2
+
+
+def test_default_stream_ordering(torch_cuda):
+    """A store given torch's default-stream handle (0) orders its launches
+    after the caller's default-stream work: an output buffer zeroed behind a
+    long-running kernel is written by the decode only after the zeroing."""
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    assert torch.cuda.current_stream().cuda_stream == 0
+    st, seqs, q = make(torch, [3000, 17], 8, 8, 128, pb.BF16, seed=12)
+    rg = [pb.Range(s, b, 0, L) for b, (s, L) in enumerate(zip(seqs, [3000, 17]))]
+    ref = decode(torch, st, rg, 2, q).clone()
+    for _ in range(3):
+        torch.cuda._sleep(200000)
+        o = torch.zeros_like(q)
+        st.decode(rg, 2, q, o)
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref)
+    st.close()
