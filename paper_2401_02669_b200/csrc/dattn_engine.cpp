@@ -251,7 +251,9 @@ void dattn_store::init(const dattn_store_config& c) {
     ma_ctas_per_sm = std::max(1, occ);
 
     // K2: tcgen05 tiles for grouped queries (bf16, d = 128, pages dividing the 128-token tile)
-    const bool tc_shape = c.dtype == kBF16 && c.head_dim == 128 && group >= 2 && group <= 16 &&
+    // MHA (group 1) too: Q is padded to the MMA's N = 16 like any group, and
+    // the tensor-core tile costs less power than K1's FFMA2 stream
+    const bool tc_shape = c.dtype == kBF16 && c.head_dim == 128 && group >= 1 && group <= 16 &&
                           (c.page_tokens == 16 || c.page_tokens == 32 || c.page_tokens == 64 ||
                            c.page_tokens == 128);
     if (tc_shape && !std::getenv("DATTN_DISABLE_TC")) {

@@ -201,7 +201,7 @@ def test_config3_gqa_shape(torch_cuda):
 
 
 @pytest.mark.parametrize("group,lens", [(8, [4096, 129, 1, 2000]), (4, [700, 3333]), (16, [1500]),
-                                        (2, [257, 64])])
+                                        (2, [257, 64]), (1, [5000, 31, 2048])])
 def test_gqa_tcgen05_path_vs_oracle_and_cuda_core_path(torch_cuda, group, lens):
     """K2 (tcgen05, swap-AB tiles) against the oracle and against K1 (CUDA
     cores) on the same store, incl. rBlocks starting mid-page and per-kv-head
@@ -458,12 +458,14 @@ def test_full_size_config4_vs_oracle_and_partition_invariance(torch_cuda):
                                  chunk=1024), 128)
     big = out_np(torch, decode(torch, st, [pb.Range(seqs[0], 0, 0, L)], 1, q, chunk=8192), 128)
     assert np.isfinite(one).all()
-    # fp32 re-association only; the outputs are stored in bf16, so one output
-    # ulp (2^-8 of the row maximum at most) is the resolution of the comparison
-    assert rel_errs(split, one) < 4e-3
-    assert rel_errs(big, one) < 4e-3
+    # K2 rounds each tile's softmax weights to bf16 relative to the running
+    # maximum, which depends on where chunks start; with bf16 outputs on top,
+    # different partitions agree to a few bf16 ulps
+    assert rel_errs(split, one) < 1e-2
+    assert rel_errs(big, one) < 1e-2
     ref = oracle.decode_ranges(44, [0], [L], [0], 32, 32, 128, dtype=pb.BF16)
-    assert rel_errs(one, ref) < 2e-2
+    for o in (one, split, big):
+        assert rel_errs(o, ref) < 2e-2
     st.close()
 
 
