@@ -316,7 +316,7 @@ def run_b200_arm(args, rank, ws, local):
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
 
-    # ---- region B: K1 alone, CUDA events around each launch on its stream ----
+    # ---- region B: the MA kernel (K1/K2) alone, CUDA events around each launch on its stream ----
     st.stats(reset=True)
     st.set_timing(True)
     kb = max(10, min(args.steps, 100))
@@ -355,7 +355,7 @@ def run_b200_arm(args, rank, ws, local):
     if rank != 0:
         return
     peak, peak_src = measured_peak()
-    # per-rank algorithmic bytes of one K1 launch (rank 0's share)
+    # per-rank algorithmic bytes of one MA launch (rank 0's share)
     kv_rank = sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in shares)
     kv_ranks = [sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in rs) for rs in workloads.rank_shares(w, ws)]
     bound_ms = max(kv_ranks) / (peak * 1e9) * 1e3
