@@ -737,7 +737,85 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             int n = 0, cbase = 0, my_kvh = 0;
             int64_t base = 0;
             if (g < groups) group_shape(g, n, cbase, base, my_kvh);
-            if (g < groups && n <= kHeavy) {
+            if (g < groups && n <= 32) {
+                // one round trip: lane c holds chunk c's header while every
+                // lane already fetches its payload words of the first chunks
+                // (independent of the weights); same arithmetic and order as
+                // fold_chunks, so the record is bit-identical
+                constexpr int kPre = (kSweeps * kVW * sizeof(Acc) <= 32) ? 4 : 1;
+                Acc hm = kNegInf, he = 0, ht = 0;
+                bool lv = false;
+                if (lane < n) {
+                    const Acc* r = R + (base + static_cast<int64_t>(lane) * p.c_stride) * REC;
+                    hm = __ldcg(r);
+                    he = __ldcg(r + 1);
+                    ht = __ldcg(r + 2);
+                    lv = ht != Acc(0);
+                    if (p.chunk_kvh) {
+                        const int tag = p.chunk_kvh[cbase + lane];
+                        if (tag >= 0 && tag != my_kvh) lv = false;
+                    }
+                }
+                Acc pre[kPre][kSweeps][kVW];
+#pragma unroll
+                for (int k = 0; k < kPre; ++k) {
+                    const Acc* r = R + (base + static_cast<int64_t>(k < n ? k : 0) * p.c_stride) * REC;
+#pragma unroll
+                    for (int sw = 0; sw < kSweeps; ++sw) {
+                        const int j = sw * kPer + lane * kVW;
+#pragma unroll
+                        for (int v = 0; v < kVW; ++v) pre[k][sw][v] = 0;
+                        if (k < n && j < DP) {
+                            if constexpr (kVW == 4) {
+                                const float4 x4 = __ldcg(reinterpret_cast<const float4*>(r + 4 + j));
+                                pre[k][sw][0] = x4.x; pre[k][sw][1] = x4.y; pre[k][sw][2] = x4.z; pre[k][sw][3] = x4.w;
+                            } else {
+#pragma unroll
+                                for (int v = 0; v < kVW; ++v) pre[k][sw][v] = __ldcg(r + 4 + j + v);
+                            }
+                        }
+                    }
+                }
+                Acc mg = lv ? hm : kNegInf;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const Acc o = __shfl_xor_sync(0xffffffffu, mg, off);
+                    mg = o > mg ? o : mg;
+                }
+                const Acc w = lv ? ((hm == mg) ? Acc(1) : exp(hm - mg)) : Acc(0);
+                Acc eg = lv ? he * w : Acc(0), ntok = lv ? ht : Acc(0);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    eg += __shfl_xor_sync(0xffffffffu, eg, off);
+                    ntok += __shfl_xor_sync(0xffffffffu, ntok, off);
+                }
+                Acc acc[kSweeps][kVW];
+#pragma unroll
+                for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) acc[sw][v] = 0;
+#pragma unroll
+                for (int k = 0; k < kPre; ++k) {
+                    const Acc wk = __shfl_sync(0xffffffffu, w, k);
+                    if (k < n)
+#pragma unroll
+                        for (int sw = 0; sw < kSweeps; ++sw)
+#pragma unroll
+                            for (int v = 0; v < kVW; ++v) acc[sw][v] += pre[k][sw][v] * wk;
+                }
+                for (int k = kPre; k < n; ++k) {
+                    const Acc wk = __shfl_sync(0xffffffffu, w, k);
+                    const Acc* r = R + (base + static_cast<int64_t>(k) * p.c_stride) * REC;
+#pragma unroll
+                    for (int sw = 0; sw < kSweeps; ++sw) {
+                        const int j = sw * kPer + lane * kVW;
+                        if (j < DP)
+#pragma unroll
+                            for (int v = 0; v < kVW; ++v) acc[sw][v] += __ldcg(r + 4 + j + v) * wk;
+                    }
+                }
+                push(g, acc, mg, eg, ntok);
+            } else if (g < groups && n <= kHeavy) {
                 auto live = [&](int c, const Acc* r) {
                     if (p.chunk_kvh) {
                         const int tag = p.chunk_kvh[cbase + c];

@@ -387,6 +387,14 @@ __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>:
     constexpr int kPer = 32 * kVW;
     constexpr int kSweeps = (DP + kPer - 1) / kPer;
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    constexpr int kPayVW = (kSweeps == 1 && kVW * sizeof(U) == 16 && DP == kPer) ? kVW : 1;
+    U pay[kMaxRanks][kPayVW];
+    if constexpr (kPayVW == kVW && kSweeps == 1 && kVW * sizeof(U) == 16 && DP == kPer) {
+#pragma unroll
+        for (int r = 0; r < kMaxRanks; ++r)
+            if (r < nranks) x_unpack<U>(ld_volatile_v4(X + (static_cast<int64_t>(r) * slot_stride + g) * REC + 4 + lane * kVW),
+                                        pay[r]);
+    }
     Acc mr = kNegInf, er = 0, tr = 0;
     if (lane < nranks) {
         U h[4];
@@ -406,23 +414,48 @@ __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>:
 #pragma unroll
         for (int v = 0; v < kVW; ++v) a2[sw][v] = 0;
     unsigned live_mask = 0;
-    for (int r = 0; r < nranks; ++r) {
-        const Acc tk = __shfl_sync(0xffffffffu, tr, r);
-        const Acc w = __shfl_sync(0xffffffffu, wl, r);
-        const Acc er_r = __shfl_sync(0xffffffffu, er, r);
-        if (tk == Acc(0)) continue;  // warp-uniform
-        live_mask |= 1u << r;
-        e2 += er_r * w;
-        tok2 += tk;
-        const U* rec = X + (static_cast<int64_t>(r) * slot_stride + g) * REC;
+    if constexpr (kSweeps == 1 && kVW * sizeof(U) == 16 && DP == kPer) {
+        // one 16-B payload word group per lane and rank: the payloads of all
+        // ranks were requested together with the headers (pay[], read once
+        // without waiting); only words not yet arrived are polled again
 #pragma unroll
-        for (int sw = 0; sw < kSweeps; ++sw) {
-            const int j = sw * kPer + lane * kVW;
-            if (j < DP) {
-                U dw[kVW];
-                x_poll<U, kVW>(rec + 4 + j, dw);
+        for (int r = 0; r < kMaxRanks; ++r) {
+            if (r < nranks) {
+                const Acc tk = __shfl_sync(0xffffffffu, tr, r);
+                const Acc w = __shfl_sync(0xffffffffu, wl, r);
+                const Acc er_r = __shfl_sync(0xffffffffu, er, r);
+                if (tk != Acc(0)) {  // warp-uniform
+                    live_mask |= 1u << r;
+                    e2 += er_r * w;
+                    tok2 += tk;
+                    bool ok = true;
 #pragma unroll
-                for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(dw[v]) * w;
+                    for (int v = 0; v < kVW; ++v) ok &= pay[r][v] != ~U(0);
+                    if (!ok) x_poll<U, kVW>(X + (static_cast<int64_t>(r) * slot_stride + g) * REC + 4 + lane * kVW, pay[r]);
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) a2[0][v] += x_dec<Acc>(pay[r][v]) * w;
+                }
+            }
+        }
+    } else {
+        for (int r = 0; r < nranks; ++r) {
+            const Acc tk = __shfl_sync(0xffffffffu, tr, r);
+            const Acc w = __shfl_sync(0xffffffffu, wl, r);
+            const Acc er_r = __shfl_sync(0xffffffffu, er, r);
+            if (tk == Acc(0)) continue;  // warp-uniform
+            live_mask |= 1u << r;
+            e2 += er_r * w;
+            tok2 += tk;
+            const U* rec = X + (static_cast<int64_t>(r) * slot_stride + g) * REC;
+#pragma unroll
+            for (int sw = 0; sw < kSweeps; ++sw) {
+                const int j = sw * kPer + lane * kVW;
+                if (j < DP) {
+                    U dw[kVW];
+                    x_poll<U, kVW>(rec + 4 + j, dw);
+#pragma unroll
+                    for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(dw[v]) * w;
+                }
             }
         }
     }
