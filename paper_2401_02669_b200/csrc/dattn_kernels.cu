@@ -699,8 +699,12 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     };
     stamp(0);
 
-    // ---- A. local merge + push to every rank
+    // ---- A. local merge + push to every rank. A group with more than
+    //      heavy_min chunk records is merged by the whole CTA: above 64
+    //      records always, above 8 when the CTA owns one group per sweep
+    //      (few groups, e.g. one long request: 7 warps would idle otherwise)
     constexpr int kHeavy = 64;
+    const int heavy_min = gpc == 1 ? 8 : kHeavy;
     auto group_shape = [&](int64_t g, int& n, int& cbase, int64_t& base, int& my_kvh) {
         const int row = static_cast<int>(g / p.heads);
         const int h = static_cast<int>(g - static_cast<int64_t>(row) * p.heads);
@@ -737,7 +741,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             int n = 0, cbase = 0, my_kvh = 0;
             int64_t base = 0;
             if (g < groups) group_shape(g, n, cbase, base, my_kvh);
-            if (g < groups && n <= 32) {
+            if (g < groups && n <= 32 && n <= heavy_min) {
                 // one round trip: lane c holds chunk c's header while every
                 // lane already fetches its payload words of the first chunks
                 // (independent of the weights); same arithmetic and order as
@@ -803,6 +807,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
 #pragma unroll
                             for (int v = 0; v < kVW; ++v) acc[sw][v] += pre[k][sw][v] * wk;
                 }
+#pragma unroll 8
                 for (int k = kPre; k < n; ++k) {
                     const Acc wk = __shfl_sync(0xffffffffu, w, k);
                     const Acc* r = R + (base + static_cast<int64_t>(k) * p.c_stride) * REC;
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
                     }
                 }
                 push(g, acc, mg, eg, ntok);
-            } else if (g < groups && n <= kHeavy) {
+            } else if (g < groups && n <= heavy_min) {
                 auto live = [&](int c, const Acc* r) {
                     if (p.chunk_kvh) {
                         const int tag = p.chunk_kvh[cbase + c];
@@ -850,7 +855,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
             int n, cbase, my_kvh;
             int64_t base;
             group_shape(g, n, cbase, base, my_kvh);
-            if (n <= kHeavy) continue;  // uniform across the CTA
+            if (n <= heavy_min) continue;  // uniform across the CTA
             auto live = [&](int c, const Acc* r) {
                 if (p.chunk_kvh) {
                     const int tag = p.chunk_kvh[cbase + c];
