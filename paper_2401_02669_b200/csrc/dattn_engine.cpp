@@ -438,6 +438,47 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     pl.any_empty_group = false;
     for (size_t i = 0; i < static_cast<size_t>(b.num_rows) * cfg.num_kv_heads; ++i)
         pl.any_empty_group |= pl.words[pl.off_expect + i] == 0;
+    // claim order: longest item first (LPT), so a ragged batch ends on short
+    // items instead of one CTA finishing a long one alone; uniform items keep
+    // the natural order (no table)
+    pl.off_table = 0;
+    if (!one_chunk_per_range && items > 1) {
+        std::vector<std::pair<int32_t, int32_t>> len_item;  // (-tokens, item)
+        len_item.reserve(static_cast<size_t>(items));
+        int32_t lmin = INT32_MAX, lmax = 0;
+        for (int i = 0; i < nr; ++i) {
+            const dattn_range& r = b.ranges[i];
+            const int64_t len = r.tok_end - r.tok_begin;
+            const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
+            const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
+            const int32_t base = pl.words[pl.off_item + i];
+            for (int64_t j = 0; j < nch; ++j) {
+                const int32_t t = static_cast<int32_t>(std::min<int64_t>(C, len - j * C));
+                lmin = std::min(lmin, t);
+                lmax = std::max(lmax, t);
+                for (int h = 0; h < nh; ++h)
+                    len_item.emplace_back(-t, base + static_cast<int32_t>(j * nh + h));
+            }
+        }
+        if (lmax > lmin) {
+            std::stable_sort(len_item.begin(), len_item.end(),
+                             [](const auto& a, const auto& b2) { return a.first < b2.first; });
+            if (pl.words.size() & 1) pl.words.push_back(0);  // 8-B aligned pairs
+            pl.off_table = pl.words.size();
+            pl.words.resize(pl.off_table + 2 * len_item.size());
+            for (size_t k = 0; k < len_item.size(); ++k) {
+                const int32_t item = len_item[k].second;
+                // range of the item: the last range whose first item <= item
+                int lo = 0, hi = nr;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) / 2;
+                    if (pl.words[pl.off_item + mid] <= item) lo = mid; else hi = mid;
+                }
+                pl.words[pl.off_table + 2 * k] = lo;
+                pl.words[pl.off_table + 2 * k + 1] = item - pl.words[pl.off_item + lo];
+            }
+        }
+    }
     pl.nitems = static_cast<int32_t>(items);
     pl.nchunks = static_cast<int32_t>(one_chunk_per_range ? nr : chunks);
     pl.nranges = nr;
@@ -507,6 +548,7 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     p.q = q_dev;
     p.ranges = reinterpret_cast<const RangeDev*>(w + pl.off_ranges);
     p.item_prefix = w + pl.off_item;
+    p.item_table = pl.off_table ? w + pl.off_table : nullptr;
     p.chunk_prefix = w + pl.off_chunk;
     p.nranges = pl.nranges;
     p.nitems = pl.nitems;

@@ -49,6 +49,7 @@ struct HostBuf {
 struct Plan {
     std::vector<int32_t> words;
     size_t off_ranges = 0, off_item = 0, off_chunk = 0, off_rowchunk = 0, off_kvh = 0, off_expect = 0;
+    size_t off_table = 0;  // 0: no claim-order table (uniform items)
     int32_t nitems = 0, nchunks = 0, nranges = 0, nrows = 0, chunk_tokens = 0;
     bool any_kvh = false;
     bool any_empty_group = false;  // some (row, kv head) has no chunk on this store

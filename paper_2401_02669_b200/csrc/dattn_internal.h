@@ -29,6 +29,7 @@ struct MAParams {
     const void* q;  // [rows][Hq][DP]
     const RangeDev* ranges;
     const int32_t* item_prefix;   // nranges+1
+    const int32_t* item_table;    // claim order: [nitems][2] = (range, local item), longest first; or null
     const int32_t* chunk_prefix;  // nranges+1
     int32_t nranges;
     int32_t nitems;

@@ -190,9 +190,16 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
             if (lane == 0) item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
             item = __shfl_sync(0xffffffffu, item, 0);
             if (item >= p.nitems) break;
-            const int r = find_range(p.item_prefix, p.nranges, item);
+            int r, local;
+            if (p.item_table) {  // longest-first claim order (one load replaces the search)
+                const int2 e = __ldg(reinterpret_cast<const int2*>(p.item_table) + item);
+                r = e.x;
+                local = e.y;
+            } else {
+                r = find_range(p.item_prefix, p.nranges, item);
+                local = item - __ldg(p.item_prefix + r);
+            }
             const RangeDev rg = p.ranges[r];
-            const int local = item - __ldg(p.item_prefix + r);
             const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
             const int j = local / nh;
             const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
