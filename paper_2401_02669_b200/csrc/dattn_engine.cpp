@@ -89,6 +89,23 @@ void dattn_store::release_exchange() {
     fused_merge = false;
 }
 
+// Order NCCL work after `stream`'s queued work, on the comm stream; comm_end()
+// orders later `stream` work after it.
+cudaStream_t dattn_store::comm_begin() {
+    if (!comm_stream) {
+        cuda_check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "cudaStreamCreate(comm)");
+        for (auto& e : comm_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    cuda_check(cudaEventRecord(comm_ev[0], stream), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(comm_stream, comm_ev[0], 0), "cudaStreamWaitEvent");
+    return comm_stream;
+}
+
+void dattn_store::comm_end() {
+    cuda_check(cudaEventRecord(comm_ev[1], comm_stream), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(stream, comm_ev[1], 0), "cudaStreamWaitEvent");
+}
+
 // Map every rank's exchange buffers into this process (CUDA IPC); the 64-byte
 // handles travel through the NCCL communicator itself.
 void dattn_store::setup_exchange() {
@@ -112,8 +129,9 @@ void dattn_store::setup_exchange() {
     cuda_check(cudaMemcpyAsync(static_cast<unsigned char*>(dh.p) + rank * kH, &hx, kH, cudaMemcpyHostToDevice,
                                stream),
                "cudaMemcpyAsync");
-    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, stream),
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, comm_begin()),
                "ncclAllGather(ipc handles)");
+    comm_end();
     cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     for (int r = 0; r < nranks; ++r) {
@@ -126,8 +144,9 @@ void dattn_store::setup_exchange() {
         cuda_check(cudaIpcOpenMemHandle(&peer_x[r], px, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
     }
     // every rank has emptied its exchange buffer before anyone can push
-    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, stream),
+    nccl_check(ncclAllGather(static_cast<unsigned char*>(dh.p) + rank * kH, dh.p, kH, ncclUint8, comm, comm_begin()),
                "ncclAllGather(barrier)");
+    comm_end();
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     epoch = 0;
     fused_merge = true;
@@ -159,6 +178,9 @@ dattn_store::~dattn_store() {
     }
     release_exchange();
     if (comm) ncclCommDestroy(comm);
+    for (auto& e : comm_ev)
+        if (e) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     for (auto* v : {&ma_events, &merge_events, &comm_events})
         for (auto& pr : *v) {
             cudaEventDestroy(pr[0]);
@@ -854,8 +876,9 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
     cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
     if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
     nccl_check(ncclAllGather(rowrecs.p, gathered.p, row_recs * rec_elems,
-                             cfg.dtype == kF64 ? ncclDouble : ncclFloat32, comm, stream),
+                             cfg.dtype == kF64 ? ncclDouble : ncclFloat32, comm, comm_begin()),
                "ncclAllGather(partials)");
+    comm_end();
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
     stats.last_exchange = 1;
     MergeParams mp{};
@@ -1319,9 +1342,11 @@ static void kv_transfer(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, in
     if (send) {
         cuda_check(launch_gather(s->cfg.dtype, s->dp, p, s->stream), "launch(gather)");
         count_launch(1);
-        nccl_check(ncclSend(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->stream), "ncclSend(kv)");
+        nccl_check(ncclSend(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->comm_begin()), "ncclSend(kv)");
+        s->comm_end();
     } else {
-        nccl_check(ncclRecv(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->stream), "ncclRecv(kv)");
+        nccl_check(ncclRecv(buf.p, 2 * bytes, ncclUint8, peer, s->comm, s->comm_begin()), "ncclRecv(kv)");
+        s->comm_end();
         cuda_check(launch_scatter(s->cfg.dtype, s->dp, p, s->stream), "launch(scatter)");
         count_launch(1);
     }

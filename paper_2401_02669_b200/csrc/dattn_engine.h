@@ -92,6 +92,14 @@ struct dattn_store {
     bool meta_valid = false;
 
     ncclComm_t comm = nullptr;
+    // NCCL runs on its own non-blocking stream, ordered with `stream` by
+    // events: a caller stream that is the legacy default stream (torch's
+    // default-stream handle) would otherwise implicitly synchronise with
+    // NCCL's internal streams
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t comm_ev[2] = {nullptr, nullptr};
+    cudaStream_t comm_begin();
+    void comm_end();
     int rank = 0, nranks = 1;
     // exchange buffers (K5 / K6): IPC-mapped, two halves used by alternate steps
     void* xbuf = nullptr;  // own [2][nranks][slot_stride][rec]
