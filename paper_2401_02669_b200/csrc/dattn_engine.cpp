@@ -833,18 +833,12 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.nranks = nranks;
         xp.slot_stride = slot_stride;
         xp.out_norm = out_dev0;
-        // 8 warps per group for long chunk lists, else one; the grid depends
-        // only on the row count and chunk shape, identical on every rank, and
-        // stays co-resident (<= 4 CTAs per SM)
-        int32_t max_row_chunks = 0;
-        for (int rr = 0; rr < b.num_rows; ++rr)
-            max_row_chunks = std::max(max_row_chunks, pl.words[pl.off_rowchunk + rr + 1] - pl.words[pl.off_rowchunk + rr]);
-        // groups per CTA iteration: 8 when groups are plentiful, else 1 so few
-        // heavy groups still spread over many CTAs -- a function of rows x heads
-        // only, hence identical on every rank. Warps per group is a local choice.
+        // groups per CTA sweep: 8 (one per warp) when groups are plentiful,
+        // else 1 so a few long groups each get a whole CTA. The grid stays
+        // co-resident (<= 4 CTAs per SM): warps polling in phase D never wait
+        // for a CTA that is not running.
         const int64_t gpc = static_cast<int64_t>(row_recs) >= 1024 ? 8 : 1;
         xp.groups_per_cta = static_cast<int32_t>(gpc);
-        xp.warps_per_group = (gpc == 1 || max_row_chunks > 64) ? 8 : 1;
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,
                                  std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));

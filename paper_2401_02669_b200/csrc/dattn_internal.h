@@ -96,8 +96,7 @@ struct XParams {
     int32_t rank;
     int32_t nranks;
     int64_t slot_stride;               // records per source rank in an exchange buffer
-    int32_t warps_per_group;           // 1 or 8 (long chunk lists); local choice
-    int32_t groups_per_cta;            // 8 or 1; identical on every rank
+    int32_t groups_per_cta;            // 8 or 1
     void* out_norm;                    // [rows*heads][DP] storage dtype
     unsigned long long* trace;         // debug (DATTN_K5_TRACE): [kMaxExchangeGrid][3] sums, else null
 };

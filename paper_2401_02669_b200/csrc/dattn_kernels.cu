@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
     const MergeParams& p = x.local;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gpc = x.groups_per_cta;  // 1 or kMergeWarps; identical on every rank
+    const int gpc = x.groups_per_cta;  // 1 or kMergeWarps
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     pdl_wait();  // launched early behind the MA grid (PDL)
