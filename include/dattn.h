@@ -107,18 +107,19 @@ dattn_status dattn_store_stream(const dattn_store* s, void** stream_out);
 dattn_status dattn_store_set_stream(dattn_store* s, void* stream);
 dattn_status dattn_store_synchronize(dattn_store* s);
 
-/* Launch statistics; with timing on, every K1 / K3 launch is bracketed by CUDA
- * events on the store stream and the device time is accumulated (bench.py's
- * roofline numerator). */
+/* Launch statistics; with timing on, every MA (K1 / K2), merge (K3) and
+ * exchange launch is bracketed by CUDA events on the store stream and the
+ * device time is accumulated (bench.py's roofline numerator). */
 typedef struct dattn_stats {
     int64_t ma_launches, merge_launches;
     int64_t ma_timed, merge_timed;
     double ma_ms, merge_ms;     /* summed device time of timed launches */
     int64_t last_items, last_chunks, last_plan_bytes;
     int32_t last_chunk_tokens, ma_grid;
-    int32_t last_kernel;        /* 1: K1 CUDA-core MA, 2: K2 tcgen05 GQA MA */
-    int32_t last_exchange;      /* 0: fused merge inside K1 (1 GPU), 1: NCCL allgather + K3,
-                                   2: K5 NVLink exchange, 3: K1 group push + K6 rank merge */
+    int32_t last_kernel;        /* 1: K1 CUDA-core MA (fp32 / fp64 / other head dims),
+                                   2: K2 tcgen05 MA (bf16, d = 128, any group 1..16) */
+    int32_t last_exchange;      /* 0: fused merge inside the MA kernel (1 GPU), 1: NCCL allgather + K3,
+                                   2: K5 NVLink exchange, 3: MA-kernel group push + K6 rank merge */
     int64_t comm_timed;
     double comm_ms;             /* summed device time of the timed exchange (allgather or K5) */
 } dattn_stats;
