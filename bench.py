@@ -2,39 +2,56 @@
 """DistAttention decode benchmark (BASELINE.json metric) -- one JSON line.
 
 Default workload: BASELINE config 2 (batch 64 decode, LLaMA2-7B MHA 32x128,
-ragged 1K-32K contexts, bf16 paged KV) on 1 B200. With --gpus N (launched by
-torch.distributed.run, one process per GPU) the SAME workload is
-sequence-sharded: every request's blocks are split into N contiguous shares
-(config 5: the gManager-policy placement), each rank runs the MA kernel over its
-share and K5 merges the (m, e, ma) partials locally, exchanges one record per
-(row, q head) over NVLink and merges across ranks (strong scaling, total work
-fixed).
+ragged 1K-32K contexts, bf16 paged KV) on 1 B200. ``--gpus N`` runs the SAME
+workload on N GPUs of this box, one process per GPU: launched by
+torch.distributed.run (the driver's way), or, when WORLD_SIZE is unset,
+re-executed by this script under torch.distributed.run itself. Every request's
+blocks are sequence-sharded (configs 1-4: equal block-aligned shares; config 5:
+the reference control plane's gManager placement, tests/golden/
+cfg5_placement.json); each rank runs the MA kernel over its share and K5 merges
+the (m, e, ma) partials locally, exchanges one record per (row, q head) over
+NVLink and merges across ranks (strong scaling: total work fixed).
 
 A step = one decode step of one attention layer for the whole batch.
-  value       tokens/s = B / t_step, inputs resident in HBM, device-timed with
-              CUDA events over exactly --steps steps (max over ranks).
-  e2e         the same through the C ABI with HOST q/out buffers: pinned H2D of
-              q + plan, D2H of the output inside every step (wall clock).
-  roofline    the MA kernel (K1 or K2, the dominant launch) timed alone with
-              CUDA events on its stream; achieved = algorithmic bytes / duration;
-              frac against the measured copy bandwidth, frac_nominal against
-              the north_star's 8 TB/s.
-  placement   per-rank KV bytes, the makespan bound they imply (max rank bytes
-              at the measured peak) and the step's fraction of it (config 5 is
-              placement-limited).
+  value        tokens/s = B / t_step, inputs resident in HBM, device-timed with
+               CUDA events over exactly --steps steps (max over ranks). The
+               batch is the same every step (KV >> L2 for configs 2-5: no flush).
+  e2e          a real decode loop through the C ABI with HOST buffers, timed
+               on the host clock around every step (max over ranks): each step
+               appends one token per request (dattn_kv_append: H2D of the new K/V
+               rows, pages allocated at page boundaries), decodes over the grown
+               contexts (the plan is rebuilt and uploaded because every range
+               grew) with q copied H2D and the output copied D2H.
+               e2e_static: the same without the append (fixed batch, plan cached).
+  parity       outside every timed region: sampled (row, q head) outputs of the
+               benchmarked step AND of the decode loop's last step against the
+               CPU oracle (oracle/, pinned to the reference by tests/golden/) on
+               identical inputs, normalised error (oracles.hpp:50-56) <= tol
+               (north_star: 2e-2 bf16, 1e-3 fp32). A failing check exits 1.
+  roofline     the MA kernel (K1 or K2, the dominant launch) timed alone with
+               CUDA events on its stream; achieved = algorithmic bytes / duration;
+               frac against the measured copy bandwidth (MEASURED_PEAKS.json),
+               frac_nominal against the north_star's 8 TB/s; traffic = DRAM
+               bytes per launch from the ncu capture of THIS library build
+               (profiles/ncu_traffic.json, keyed by the library's sha256).
+  placement    per-rank KV bytes, the makespan bound they imply (max rank bytes
+               at the measured peak) and the step's fraction of it (config 5 is
+               placement-limited).
   cpu_baseline the reference's own multi_head_attention (oracle/_ref, compiled
-              from the unmodified sources) on all host cores, bounded sample;
-              single_thread_value = the same on 1 core (as shipped).
-  model_tps   B / (n_layers * t_step), the reference's TPS = beta/(n T_layer)
-              (perfmodel.cpp:120-130) for the workload's model depth.
---impl reference times only that CPU reference (rank 0) and prints its line.
+               from the unmodified sources) on all host cores, bounded sample;
+               single_thread_value = the same on 1 core (as shipped).
+  model_tps    B / (n_layers * t_step), the reference's TPS = beta/(n T_layer)
+               (perfmodel.cpp:120-130) for the workload's model depth.
+--impl reference times only that CPU reference (rank 0) and prints its line;
+it never loads the product library.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,6 +62,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode-attention tokens/s and KV GB/s (% HBM roofline) at 1/2/4/8 B200 vs CPU"
+_JSON_OUT = sys.stdout  # main() points it at the real stdout; everything else goes to stderr
+
+
+def emit(line: dict) -> None:
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+TOL = {0: 2e-2, 1: 1e-3}  # north_star: bf16 2e-2, fp32 1e-3 (normalised error)
 
 
 def parse():
@@ -54,10 +78,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="2", help="BASELINE config number (1..5)")
+    ap.add_argument("--cfg5-queue", type=int, default=64,
+                    help="config 5: debtor queue of the reference placement (0, 64 or 512)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="decode-loop steps (0: min(--steps, 64))")
     ap.add_argument("--chunk-tokens", type=int, default=0)
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check (profiling runs)")
     return ap.parse_args()
 
 
@@ -68,6 +95,30 @@ def measured_peak():
         return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def repo_libs_loaded():
+    """Shared objects of this repo mapped into the process (evidence of which
+    library a measurement ran through)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            p = line.split()[-1]
+            if p.endswith(".so") and p.startswith(ROOT):
+                libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 class ClockSampler:
@@ -88,7 +139,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -97,7 +148,7 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -109,28 +160,33 @@ class ClockSampler:
             if len(parts) < 9:
                 continue
             try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
             except ValueError:
                 continue
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
-        loaded = [c for c, _, _ in rows]
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({names[i] for _, _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
+        # samples under load: power above the idle floor (the first and last
+        # samples bracket the region and may be idle)
+        pmax = max(p for _, _, p, _ in rows)
+        loaded = [c for c, _, p, _ in rows if p >= 0.5 * pmax] or [c for c, _, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _, _ in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": pmax}
 
 
 # ----------------------------------------------------------------- CPU side
 
-def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int = 0):
+def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int = 0, warmup: int = 0):
     """Time the reference CPU path on a bounded sample of the workload.
 
     The sample is the first requests of the batch (all their heads), generated
     with the same counter-hash values the GPU consumes (bf16-rounded, then
     widened to fp64: the reference API is fp64-only). Generation is outside
-    the timed region. Returns the full-workload-equivalent tokens/s and info.
+    the timed region; ``warmup`` untimed reps precede the timed ones. Returns
+    the full-workload-equivalent tokens/s and info.
     """
     import ctypes
     from concurrent.futures import ThreadPoolExecutor
@@ -185,6 +241,8 @@ def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int =
                             seg_tokens=seg, threads=threads)
         return time.perf_counter() - t0
 
+    for _ in range(max(warmup, 0)):
+        one()
     times = []
     t_start = time.perf_counter()
     while True:
@@ -198,7 +256,8 @@ def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int =
     full_tok_heads = w.total_tokens * w.hkv
     full_t = per * full_tok_heads / sample_tok_heads
     info = {
-        "kind": kind, "cores": threads, "reps": len(times), "sample_seconds_per_rep": per,
+        "kind": kind, "cores": threads, "reps": len(times), "warmup_reps": max(warmup, 0),
+        "sample_seconds_per_rep": per, "cpu_model": cpu_model(),
         "sample": (f"{B} leading request(s) of the batch, {sum(lens)} context tokens x {w.hkv} kv heads "
                    f"({sum(lens) * w.hkv * w.d * 16 / 1e9:.2f} GB fp64 K+V), kvsched::attn::multi_head_attention "
                    f"per (request, kv head) on {threads} threads; scaled to the full workload by K/V tokens "
@@ -209,15 +268,16 @@ def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int =
 
 
 def run_reference_arm(args, rank, ws):
+    # workloads is pure host code: importing it does not map libdattn.so
     from paper_2401_02669_b200 import workloads
     if rank != 0:
         return
-    w = workloads.config(args.config)
-    for _ in range(max(args.warmup, 0)):
-        pass  # warm-up reps are counted inside cpu_reference_sample via reps_fixed below
-    total_reps = max(args.steps, 1) + max(args.warmup, 0)
-    # each step: one bounded-sample rep; keep the whole run to a few minutes
-    value, info = cpu_reference_sample(w, budget_s=0.0, reps_fixed=min(total_reps, 60))
+    w = workloads.config(args.config, args.cfg5_queue)
+    # each step is one bounded-sample rep; keep the whole run to a few minutes
+    reps = min(max(args.steps, 1), 60)
+    value, info = cpu_reference_sample(w, budget_s=0.0, reps_fixed=reps, warmup=min(max(args.warmup, 0), 3))
+    libs = repo_libs_loaded()
+    assert not any("libdattn" in x for x in libs), libs  # the reference arm never maps the product
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * w.batch / value,
@@ -226,14 +286,95 @@ def run_reference_arm(args, rank, ws):
         "config": {"workload": w.name, "batch": w.batch, "total_kv_tokens": w.total_tokens,
                    "heads": [w.hq, w.hkv], "head_dim": w.d, **w.meta},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": info["cores"], "kind": info["kind"],
-                         "sample": info["sample"] + f"; {info['reps']} reps (steps capped at 60)"},
+                         "cpu_model": info["cpu_model"],
+                         "sample": info["sample"] + f"; {info['warmup_reps']} untimed + {info['reps']} timed reps "
+                                                    f"(timed reps capped at 60)"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "kv_gbs_fp64": info["kv_gbs_fp64"],
+        "libs_loaded": libs,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# ----------------------------------------------------------------- parity
+
+def sample_rows(w, max_rows: int = 8):
+    """Rows checked against the oracle: all of a small batch, else the first,
+    the last, the longest, the shortest and seeded picks."""
+    import random
+    B = w.batch
+    if B <= max_rows:
+        return list(range(B))
+    rows = {0, B - 1, max(range(B), key=lambda r: w.lens[r]), min(range(B), key=lambda r: w.lens[r])}
+    rng = random.Random(w.seed)
+    while len(rows) < max_rows:
+        rows.add(rng.randrange(B))
+    return sorted(rows)
+
+
+def parity_check(w, out_host, lens, budget_tok_heads: float = 4e6):
+    """Sampled (row, kv head) groups of ``out_host`` [B][Hq][dp] (the output of
+    the benchmarked step over contexts ``lens``) against the CPU oracle on the
+    same inputs. Returns the JSON object (``pass`` false when over tol)."""
+    import random
+
+    import numpy as np
+
+    import oracle
+    t0 = time.perf_counter()
+    rows = sample_rows(w)
+    g = w.hq // w.hkv
+    cost = 1.0 + g / 2.0  # K/V generation + g q heads of compute per token
+    rng = random.Random(w.seed ^ 0x5A5A)
+    # the oracle's batch index is the query row and the logical sequence, as
+    # on the GPU: pass every row up to the last checked one, select only the
+    # sampled (row, kv head) pairs (the others are skipped, not computed)
+    nb = rows[-1] + 1
+    sel = np.zeros((nb, w.hkv), dtype=bool)
+    per_row = budget_tok_heads / len(rows)
+    for r in rows:
+        k = int(max(1, min(w.hkv, per_row // max(lens[r] * cost, 1))))
+        for h in sorted(rng.sample(range(w.hkv), k)):
+            sel[r, h] = True
+    ref = oracle.decode_ranges(w.seed, [0] * nb, [lens[r] if r in rows else 0 for r in range(nb)], list(range(nb)),
+                               w.hq, w.hkv, w.d, dtype=w.dtype, amp_k=w.amp_k, amp_v=w.amp_v, select=sel)
+    err = 0.0
+    heads = 0
+    finite = True
+    for r in rows:
+        for kvh in np.nonzero(sel[r])[0]:
+            for h in range(kvh * g, (kvh + 1) * g):
+                got = np.asarray(out_host[r, h, :w.d], dtype=np.float64)
+                finite &= bool(np.isfinite(got).all())
+                err = max(err, oracle.rel_err(got, ref[r, h]))
+                heads += 1
+    tol = TOL[w.dtype]
+    return {"max_norm_err": err, "tol": tol, "pass": bool(finite and err <= tol), "rows_checked": rows,
+            "row_heads_checked": heads, "of_row_heads": w.batch * w.hq,
+            "metric": "max |got-ref| / max |ref| per (row, q head) (proj/tests/oracles.hpp:50-56)",
+            "oracle": "oracle/dattn_oracle.c fp64 (pinned to the reference: tests/golden/)",
+            "seconds": round(time.perf_counter() - t0, 2)}
 
 
 # ----------------------------------------------------------------- GPU side
+
+def traffic_for(key: str):
+    """DRAM bytes per launch of the dominant kernel from profiles/ncu_traffic.json,
+    only when that capture was made on this exact library build."""
+    import paper_2401_02669_b200 as pb
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        j = json.load(open(tf))
+        ent = j.get(key)
+        sha = hashlib.sha256(open(pb.LIB_PATH, "rb").read()).hexdigest()
+    except Exception:
+        return None, "no capture"
+    if not isinstance(ent, dict):
+        return None, "no capture for this config"
+    if ent.get("lib_sha256") != sha:
+        return None, f"capture of another build ({ent.get('git_head', '?')}); not reported"
+    return ent.get("traffic"), f"ncu --set full, {ent.get('kernel')}, build {ent.get('git_head', '?')}"
+
 
 def run_b200_arm(args, rank, ws, local):
     import numpy as np
@@ -243,19 +384,33 @@ def run_b200_arm(args, rank, ws, local):
     import paper_2401_02669_b200 as pb
     from paper_2401_02669_b200 import workloads
 
-    w = workloads.config(args.config)
+    w = workloads.config(args.config, args.cfg5_queue)
     torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
     page = w.page_tokens
-    shares = workloads.rank_shares(w, ws)[rank]
-    pages = sum(-(-rr.tokens // page) for rr in shares) + 16
-    max_pps = max(-(-rr.tokens // page) for rr in shares) + 2
+    all_shares = workloads.rank_shares(w, ws)
+    shares = all_shares[rank]
+    # decode loop: every request grows by one token per e2e step, on the rank
+    # that holds its last token (the tail)
+    ke = args.e2e_steps or min(args.steps, 64)
+    grow_total = ke + 3
+    tail_rank = {}
+    for r_, rs in enumerate(all_shares):
+        for rr in rs:
+            if rr.tokens and rr.tok_end == w.lens[rr.request]:
+                tail_rank[rr.request] = r_
+    mine = [rr.request in tail_rank and tail_rank[rr.request] == rank for rr in shares]
+    cap_tokens = [rr.tokens + (grow_total if m else 0) for rr, m in zip(shares, mine)]
+    pages = sum(-(-t // page) for t in cap_tokens) + 16
+    max_pps = max(-(-t // page) for t in cap_tokens) + 2
     st = pb.Store(w.d, w.hq, w.hkv, w.dtype, page, pages, max_seqs=w.batch + 4,
                   max_pages_per_seq=max(max_pps, 1), device=local)
     stream = torch.cuda.Stream(device=local)
     st.set_stream(stream.cuda_stream)
-    ranges = []
+    seqs, ranges = [], []
     for rr in shares:
         seq = st.seq_create(rr.tokens)
+        seqs.append(seq)
         st.fill_synthetic(seq, w.seed, rr.request, rr.tok_begin, w.amp_k, w.amp_v)
         if rr.tokens == 0:
             ranges.append(pb.Range(seq, rr.request, 0, 0))
@@ -264,21 +419,28 @@ def run_b200_arm(args, rank, ws, local):
         cuts = [rr.tokens * i // nb for i in range(nb + 1)]
         for a, b in zip(cuts[:-1], cuts[1:]):
             ranges.append(pb.Range(seq, rr.request, a, b))
-    ranges = pb.range_array(ranges)  # packed once, reused by every step
+    franges = pb.range_array(ranges)  # packed once, reused by every step
     tdt = {0: torch.bfloat16, 1: torch.float32}[w.dtype]
-    q = torch.empty(w.batch, w.hq, st.padded_dim, dtype=tdt, device=f"cuda:{local}")
+    q = torch.empty(w.batch, w.hq, st.padded_dim, dtype=tdt, device=dev)
     st.q_fill_synthetic(q, w.batch, w.seed, 0, 1.0)
     out = torch.empty_like(q)
+    comm = None
     if ws > 1:
         uid = [pb.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         st.comm_init(uid[0], rank, ws)
+        crank, cn, xmode = st.comm_info()
+        comm = {"nccl_rank": crank, "nccl_nranks": cn,
+                "exchange": {1: "ncclAllGather + K3", 2: "K5 NVLink exchange", 3: "K1/K2 push + K6"}[xmode]}
+        print(f"[bench rank {rank}] NCCL communicator: rank {crank} of {cn} (ncclCommCount); "
+              f"exchange: {comm['exchange']}", file=sys.stderr, flush=True)
+        assert crank == rank and cn == ws, comm
 
-    def step(mem=pb.MEM_DEVICE, qq=q, oo=out):
+    def step(rg=franges, mem=pb.MEM_DEVICE, qq=q, oo=out):
         if ws > 1:
-            st.decode_sharded(ranges, w.batch, qq, oo, mem=mem, chunk_tokens=args.chunk_tokens)
+            st.decode_sharded(rg, w.batch, qq, oo, mem=mem, chunk_tokens=args.chunk_tokens)
         else:
-            st.decode(ranges, w.batch, qq, oo, mem=mem, chunk_tokens=args.chunk_tokens)
+            st.decode(rg, w.batch, qq, oo, mem=mem, chunk_tokens=args.chunk_tokens)
 
     def barrier():
         if ws > 1:
@@ -287,7 +449,7 @@ def run_b200_arm(args, rank, ws, local):
     def max_over_ranks(x: float) -> float:
         if ws == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -315,6 +477,7 @@ def run_b200_arm(args, rank, ws, local):
     clocks = sampler.stop()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
+    out_a = out.cpu()
 
     # ---- region B: the MA kernel (K1/K2) alone, CUDA events around each launch on its stream ----
     st.stats(reset=True)
@@ -334,40 +497,97 @@ def run_b200_arm(args, rank, ws, local):
         dist.all_gather_object(rank_times, [ma_ms, comm_ms])
     kernel_name = {1: "ma_decode_kernel (K1, CUDA cores)", 2: "gqa_tc_kernel (K2, tcgen05)"}.get(s.last_kernel, "?")
 
-    # ---- region C: end to end through the C ABI with host buffers ----
+    # ---- region C: static e2e (fixed batch) through the C ABI with host buffers ----
     qh = q.cpu().pin_memory()
     oh = torch.empty_like(qh).pin_memory()
-    ke = args.e2e_steps or args.steps
     for _ in range(3):
-        step(pb.MEM_HOST, qh, oh)
+        step(mem=pb.MEM_HOST, qq=qh, oo=oh)
     barrier()
     t0 = time.perf_counter()
     for _ in range(ke):
-        step(pb.MEM_HOST, qh, oh)
-    t_e2e = max_over_ranks(time.perf_counter() - t0) / ke
-    plan_bytes = st.stats().last_plan_bytes
-    qbytes = qh.numel() * qh.element_size()
+        step(mem=pb.MEM_HOST, qq=qh, oo=oh)
+    t_static = max_over_ranks(time.perf_counter() - t0) / ke
+    static_same = bool(torch.equal(oh, out_a))
 
-    # parity spot check of the benchmarked output (one request, all heads) is
-    # done by tests/; here only a sanity check that the output is finite
-    assert torch.isfinite(out.float()).all().item()
+    # ---- region D: the decode loop, end to end ----
+    # inputs of every step, made before the region: the new token's K/V rows
+    # (the generator's values at position L_r + t, so the oracle can check the
+    # result) in pinned host memory, [step][my tail requests][Hkv][dp]
+    app_idx = [i for i, m in enumerate(mine) if m]
+    app_seqs = [seqs[i] for i in app_idx]
+    n_app = len(app_idx)
+    lens_now = list(w.lens)
+    kh = vh = None
+    if n_app:
+        kd = torch.empty(grow_total, n_app, w.hkv, st.padded_dim, dtype=tdt, device=dev)
+        vd = torch.empty_like(kd)
+        for t in range(grow_total):
+            st.synthetic_rows([shares[i].request for i in app_idx], [w.lens[shares[i].request] + t for i in app_idx],
+                              w.seed, kd[t], vd[t], w.amp_k, w.amp_v)
+        kh = kd.cpu().pin_memory()
+        vh = vd.cpu().pin_memory()
+        del kd, vd
+    cur_end = [rr.tokens for rr in shares]
+
+    brk = [0.0, 0.0, 0.0]  # host seconds in append / range build / decode call
+
+    def loop_step(t):
+        c0 = time.perf_counter()
+        if n_app:
+            st.kv_append(app_seqs, kh[t], vh[t], mem=pb.MEM_HOST)
+            for i in app_idx:
+                cur_end[i] += 1
+        c1 = time.perf_counter()
+        # every range of a request ends at its current length (ws > 1: one
+        # range per request per rank; ws == 1: rBlock cuts, the last one grows)
+        rg = []
+        for i, rr in enumerate(shares):
+            if ws > 1 or w.rblocks == 1:
+                rg.append(pb.Range(seqs[i], rr.request, 0, cur_end[i]))
+            else:
+                cuts = [rr.tokens * j // w.rblocks for j in range(w.rblocks)] + [cur_end[i]]
+                rg.extend(pb.Range(seqs[i], rr.request, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
+        c2 = time.perf_counter()
+        step(rg=rg, mem=pb.MEM_HOST, qq=qh, oo=oh)
+        c3 = time.perf_counter()
+        brk[0] += c1 - c0
+        brk[1] += c2 - c1
+        brk[2] += c3 - c2
+
+    for t in range(3):  # warm-up steps grow the contexts too
+        loop_step(t)
+    st.stats(reset=True)
+    brk[:] = [0.0, 0.0, 0.0]
+    barrier()
+    t0 = time.perf_counter()
+    for t in range(3, 3 + ke):
+        loop_step(t)
+    t_loop = max_over_ranks(time.perf_counter() - t0) / ke
+    plan_bytes = st.stats().last_plan_bytes
+    lens_now = [L + grow_total for L in w.lens]
+    out_d = oh.clone()
+    qbytes = qh.numel() * qh.element_size()
+    app_bytes = 2 * n_app * w.hkv * st.padded_dim * st.elem_bytes
+
+    # ---- parity of what was timed (outside every timed region) ----
+    parity = parity_loop = None
+    if rank == 0 and not args.no_parity:
+        parity = parity_check(w, out_a.float().numpy() if w.dtype == 0 else out_a.numpy(), w.lens)
+        parity["e2e_static_bitwise_equal"] = static_same
+        parity["pass"] = parity["pass"] and static_same
+        parity_loop = parity_check(w, out_d.float().numpy() if w.dtype == 0 else out_d.numpy(), lens_now)
+        parity_loop["context_tokens_after_loop"] = sum(lens_now)
 
     if rank != 0:
-        return
+        return 0
     peak, peak_src = measured_peak()
     # per-rank algorithmic bytes of one MA launch (rank 0's share)
     kv_rank = sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in shares)
-    kv_ranks = [sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in rs) for rs in workloads.rank_shares(w, ws)]
+    kv_ranks = [sum(2 * w.hkv * w.d * rr.tokens * w.elem_bytes for rr in rs) for rs in all_shares]
     bound_ms = max(kv_ranks) / (peak * 1e9) * 1e3
     alg_rank = kv_rank + w.batch * w.hq * w.d * 2 * w.elem_bytes
     achieved = alg_rank / (ma_ms * 1e-3) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get(f"cfg{args.config}_n{ws}")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = traffic_for(f"cfg{args.config}_n{ws}")
     value = w.batch / (ms_step * 1e-3)
     line = {
         "impl": "b200", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
@@ -384,43 +604,94 @@ def run_b200_arm(args, rank, ws, local):
         "model_tps": {"value": value / w.n_layers, "n_layers": w.n_layers},
         "rank0_kv_bytes": kv_rank,
         "placement": {"per_rank_kv_bytes": kv_ranks, "bound_ms": bound_ms, "frac": bound_ms / ms_step,
+                      "balanced_bound_ms": w.kv_bytes() / ws / (peak * 1e9) * 1e3,
                       "aggregate_frac": w.kv_bytes() / (ws * peak * 1e9) / (ms_step * 1e-3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "frac_nominal": achieved / 8000.0,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "frac_nominal": achieved / 8000.0,
                      "kernel": kernel_name, "kernel_ms": ma_ms, "merge_ms": merge_ms, "exchange_ms": comm_ms,
                      "alg_bytes_per_launch": alg_rank, "peak_source": peak_src},
-        "e2e": {"value": w.batch / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": qbytes + plan_bytes,
-                "d2h_bytes_per_step": qbytes, "ms_per_step": t_e2e * 1e3},
+        "e2e": {"value": w.batch / t_loop, "unit": "tokens/s",
+                "h2d_bytes_per_step": qbytes + app_bytes + plan_bytes, "d2h_bytes_per_step": qbytes,
+                "ms_per_step": t_loop * 1e3, "steps": ke,
+                "what": "decode loop through the C ABI, host clock, max over ranks: per step dattn_kv_append of "
+                        "one token per request (H2D of its K/V rows) + decode over the grown contexts "
+                        "(plan rebuilt and uploaded) with H2D q and D2H output",
+                "h2d_split": {"q": qbytes, "kv_rows_rank0": app_bytes, "plan_rank0": plan_bytes},
+                "host_ms_rank0": {"kv_append_call": 1e3 * brk[0] / ke, "range_build": 1e3 * brk[1] / ke,
+                                  "decode_call": 1e3 * brk[2] / ke}},
+        "e2e_static": {"value": w.batch / t_static, "unit": "tokens/s", "ms_per_step": t_static * 1e3,
+                       "h2d_bytes_per_step": qbytes, "d2h_bytes_per_step": qbytes,
+                       "what": "fixed batch repeated (plan cached), H2D q + D2H output"},
+        "parity": parity, "parity_decode_loop": parity_loop,
         "gpu_launches": launches,
         "per_rank_ms": {"ma": [round(t[0], 4) for t in rank_times],
                         "exchange": [None if t[1] is None else round(t[1], 4) for t in rank_times]},
         "clocks": clocks,
+        "libs_loaded": repo_libs_loaded(),
     }
+    if comm:
+        line["comm"] = comm
     if ws == 1 and not args.no_cpu_baseline:
         cv, info = cpu_reference_sample(w, args.cpu_seconds)
         c1, info1 = cpu_reference_sample(w, min(args.cpu_seconds, 4.0), threads=1)
         line["cpu_baseline"] = {"value": cv, "unit": "tokens/s", "cores": info["cores"], "kind": info["kind"],
+                                "cpu_model": info["cpu_model"],
                                 "sample": info["sample"] + f"; {info['reps']} reps",
                                 "single_thread_value": c1, "single_thread_reps": info1["reps"],
                                 "kv_gbs_fp64": info["kv_gbs_fp64"], "single_thread_kv_gbs_fp64": info1["kv_gbs_fp64"]}
-    print(json.dumps(line), flush=True)
+    emit(line)
+    ok = all(p is None or p["pass"] for p in (parity, parity_loop))
+    if not ok:
+        print("[bench] PARITY FAILED: " + json.dumps({"parity": parity, "parity_decode_loop": parity_loop}),
+              file=sys.stderr, flush=True)
+    return 0 if ok else 1
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(n: int) -> int:
+    """Re-run this command as N ranks under torch.distributed.run (one process
+    per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, stdout=_JSON_OUT)
 
 
 def main():
+    global _JSON_OUT
     args = parse()
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    # stdout carries exactly the one JSON line: libraries that print to
+    # stdout (NCCL's version banner, torch.distributed.run) go to stderr
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    ws_env = os.environ.get("WORLD_SIZE")
+    ws = int(ws_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank, ws)
-        return
+        return 0
+    if ws_env is None and args.gpus > 1:
+        return self_launch(args.gpus)
+    if ws != args.gpus:
+        print(f"[bench] refusing: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr, flush=True)
+        return 2
     if ws > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     try:
-        run_b200_arm(args, rank, ws, local)
+        return run_b200_arm(args, rank, ws, local)
     finally:
         if ws > 1:
             import torch.distributed as dist
@@ -428,4 +699,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

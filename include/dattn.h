@@ -158,11 +158,23 @@ dattn_status dattn_kv_read(dattn_store* s, int32_t seq, int kv_head, int64_t tok
 
 /* KV append (the decode loop's write): every sequence in
  * seqs[0..n) grows by one token (a page is allocated when the last one is
- * full, RManager::alloc_local controlplane.cpp:38-44) and the new rows
- * k_new/v_new [n][num_kv_heads][padded_dim] (store dtype, `mem` memory) are
- * written at the new position. seqs is a HOST array. */
+ * full, RManager::alloc_local controlplane.cpp:38-44; the pages of the whole
+ * batch are checked first, so DATTN_ERR_CAPACITY leaves the ledger unchanged)
+ * and the new rows k_new/v_new [n][num_kv_heads][padded_dim] (store dtype,
+ * `mem` memory) are written at the new position. seqs is a HOST array.
+ * Asynchronous on the store stream: HOST rows are read like cudaMemcpyAsync
+ * reads them, so keep them unchanged until the next synchronising call (a
+ * HOST-memory decode or dattn_store_synchronize). */
 dattn_status dattn_kv_append(dattn_store* s, int n, const int32_t* seqs, const void* k_new,
                              const void* v_new, int mem);
+
+/* Synthetic K/V rows [n][num_kv_heads][padded_dim] (store dtype, DEVICE
+ * k_dev/v_dev) of logical sequence logical_seqs[i], token logical_toks[i]:
+ * the values K4 writes at those positions, i.e. decode-loop inputs whose
+ * result the CPU oracle can check (HOST index arrays; synchronous). */
+dattn_status dattn_kv_synthetic_rows(dattn_store* s, int n, const uint32_t* logical_seqs,
+                                     const int64_t* logical_toks, uint64_t seed, float amp_k, float amp_v,
+                                     void* k_dev, void* v_dev);
 
 /* K4: deterministic counter-hash fill of ALL heads of tokens [0, tokens(seq))
  * of `seq` with the values of logical sequence `logical_seq`, logical token
@@ -260,6 +272,19 @@ dattn_status dattn_merge_partials(dattn_store* s, const dattn_merge_desc* d, con
 dattn_status dattn_comm_unique_id(unsigned char id[DATTN_UNIQUE_ID_BYTES]);
 dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE_ID_BYTES],
                              int rank, int nranks);
+/* Make every rank-merge poll of this store give up (K5 phase D / K6 return
+ * instead of waiting; dattn_store_synchronize and the next
+ * dattn_decode_sharded then fail with DATTN_ERR_NCCL). Polls also give up by
+ * themselves after DATTN_EXCHANGE_TIMEOUT_S seconds (environment, default 60)
+ * without a peer's record, instead of trapping, so a rank that failed before
+ * launching never kills its peers' CUDA contexts. dattn_comm_init rebuilds
+ * the exchange. Safe to call from another host thread while a step runs. */
+dattn_status dattn_comm_abort(dattn_store* s);
+/* The communicator as NCCL reports it (ncclCommUserRank / ncclCommCount) and
+ * the exchange decode_sharded will use: 1 ncclAllGather + K3, 2 K5 NVLink
+ * exchange, 3 MA-kernel push + K6. Fails with DATTN_ERR_CONTRACT before
+ * dattn_comm_init. */
+dattn_status dattn_comm_info(const dattn_store* s, int* rank, int* nranks, int* exchange);
 /* q/out as in dattn_decode; every rank passes the same num_rows. */
 dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const void* q,
                                   void* out, int mem);

@@ -64,6 +64,10 @@ def _load_oracle():
         "or_decode_ranges": (ctypes.c_int, [U64, ctypes.c_int, VP, VP, VP, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, D, ctypes.c_int, ctypes.c_float,
                                             ctypes.c_float, ctypes.c_float, ctypes.c_int, VP, VP, VP]),
+        "or_decode_ranges_sel": (ctypes.c_int, [U64, ctypes.c_int, VP, VP, VP, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, D, ctypes.c_int, ctypes.c_float,
+                                                ctypes.c_float, ctypes.c_float, VP, ctypes.c_int, VP, VP,
+                                                VP]),
     }
     for n, (r, a) in sig.items():
         f = getattr(lib, n)
@@ -189,8 +193,11 @@ def synth_q(seed: int, row: int, head: int, d: int, amp_q=1.0, dtype: int = BF16
 
 def decode_ranges(seed: int, tok_lo: Sequence[int], tok_hi: Sequence[int], seq_ids: Sequence[int],
                   hq: int, hkv: int, d: int, scale: float = 0.0, dtype: int = BF16,
-                  amp_q=1.0, amp_k=1.0, amp_v=2.0, threads: int = 0, want_me: bool = False):
-    """fp64 reference output [B, hq, d] of every request over [tok_lo, tok_hi)."""
+                  amp_q=1.0, amp_k=1.0, amp_v=2.0, threads: int = 0, want_me: bool = False,
+                  select=None):
+    """fp64 reference output [B, hq, d] of every request over [tok_lo, tok_hi).
+    ``select``: optional boolean [B, hkv] -- compute only those (request, kv
+    head) pairs (all q heads of each group); other outputs stay zero."""
     B = len(tok_lo)
     lo = np.ascontiguousarray(tok_lo, dtype=np.int64)
     hi = np.ascontiguousarray(tok_hi, dtype=np.int64)
@@ -199,8 +206,13 @@ def decode_ranges(seed: int, tok_lo: Sequence[int], tok_hi: Sequence[int], seq_i
     m = np.zeros((B, hq)) if want_me else None
     e = np.zeros((B, hq)) if want_me else None
     threads = threads or (os.cpu_count() or 1)
-    lib.or_decode_ranges(seed, B, _p(lo), _p(hi), _p(ids), hq, hkv, d, scale, dtype, amp_q, amp_k,
-                         amp_v, threads, _p(out), _p(m), _p(e))
+    if select is None:
+        lib.or_decode_ranges(seed, B, _p(lo), _p(hi), _p(ids), hq, hkv, d, scale, dtype, amp_q, amp_k,
+                             amp_v, threads, _p(out), _p(m), _p(e))
+    else:
+        sel = np.ascontiguousarray(np.asarray(select, dtype=bool).reshape(B, hkv), dtype=np.uint8)
+        lib.or_decode_ranges_sel(seed, B, _p(lo), _p(hi), _p(ids), hq, hkv, d, scale, dtype, amp_q, amp_k,
+                                 amp_v, _p(sel), threads, _p(out), _p(m), _p(e))
     return (out, m, e) if want_me else out
 
 
@@ -249,6 +261,10 @@ def ref():
                                  I64, ctypes.c_int, VP, VP],
             "ref_default_config_json": [ctypes.c_int, I64, ctypes.POINTER(ctypes.c_void_p)],
             "ref_config_eval": [ctypes.c_char_p, ctypes.c_int, VP, VP, I64, VP, VP, VP],
+            "ref_blocks_for_tokens": [I64, ctypes.c_int, VP],
+            "ref_rmanager_trace": [I64, ctypes.c_int, VP, VP, VP, VP, VP, VP, VP, VP],
+            "ref_cfg5_place": [ctypes.c_int, I64, I64, ctypes.c_int, ctypes.c_int, VP, VP, VP,
+                               ctypes.c_int, VP, VP, VP],
         }.items():
             f = getattr(r, n)
             f.restype = ctypes.c_int
@@ -286,3 +302,56 @@ def ref_config_eval(text: str, xs: Sequence[float], ctx_lengths: Sequence[int]):
     if rc != 0:
         raise ValueError(r.ref_last_error().decode())
     return g, float(lt[0]), int(nl[0])
+
+
+# ---- the reference ledger and control plane ----
+def ref_blocks_for_tokens(tokens: int, block: int) -> int:
+    """kvsched::perf::blocks_for_tokens (perfmodel.cpp:178-182), compiled."""
+    r = ref()
+    out = np.zeros(1, dtype=np.int64)
+    if r.ref_blocks_for_tokens(tokens, block, _p(out)) != 0:
+        raise ValueError(r.ref_last_error().decode())
+    return int(out[0])
+
+
+LEDGER_ALLOC_LOCAL, LEDGER_ALLOC_HOSTED, LEDGER_FREE = 0, 1, 2
+
+
+def ref_rmanager_trace(capacity: int, ops):
+    """Run ``ops`` = [(op, req, n, home)] through one reference RManager
+    (controlplane.cpp:38-79). Returns per-op (result, used, free, local)."""
+    r = ref()
+    k = len(ops)
+    op = np.ascontiguousarray([o[0] for o in ops], dtype=np.int32)
+    req = np.ascontiguousarray([o[1] for o in ops], dtype=np.int64)
+    n = np.ascontiguousarray([o[2] for o in ops], dtype=np.int64)
+    n2 = np.ascontiguousarray([o[3] if len(o) > 3 else -1 for o in ops], dtype=np.int32)
+    res, used, free, local = (np.zeros(max(k, 1), dtype=np.int64) for _ in range(4))
+    rc = r.ref_rmanager_trace(capacity, k, _p(op), _p(req), _p(n), _p(n2), _p(res), _p(used), _p(free),
+                              _p(local))
+    if rc != 0:
+        raise ValueError(r.ref_last_error().decode())
+    return [(int(res[i]), int(used[i]), int(free[i]), int(local[i])) for i in range(k)]
+
+
+def ref_cfg5_place(tokens: Sequence[int], n_inst: int, capacity_blocks: int, queued: int, rounds: int = 1):
+    """Config-5 placement by the reference control plane (ref_bridge.cpp
+    ref_cfg5_place): dispatch, heartbeats, GManager::plan + execute_move_sync.
+    Returns (homes, blocks[req][inst], moves) with moves as dicts."""
+    r = ref()
+    n_req = len(tokens)
+    t = np.ascontiguousarray(tokens, dtype=np.int64)
+    home = np.zeros(n_req, dtype=np.int32)
+    blocks = np.zeros(n_req * n_inst, dtype=np.int64)
+    maxm = 256
+    moves = np.zeros(6 * maxm, dtype=np.int64)
+    gains = np.zeros(maxm)
+    nm = np.zeros(1, dtype=np.int32)
+    rc = r.ref_cfg5_place(n_inst, capacity_blocks, queued, rounds, n_req, _p(t), _p(home), _p(blocks), maxm,
+                          _p(moves), _p(gains), _p(nm))
+    if rc != 0:
+        raise ValueError(r.ref_last_error().decode())
+    mv = [dict(round=int(moves[6 * i]), req_id=int(moves[6 * i + 1]), src_instance=int(moves[6 * i + 2]),
+               dst_instance=int(moves[6 * i + 3]), num_blocks=int(moves[6 * i + 4]),
+               moved_blocks=int(moves[6 * i + 5]), est_gain=float(gains[i])) for i in range(min(int(nm[0]), maxm))]
+    return [int(h) for h in home], blocks.reshape(n_req, n_inst).tolist(), mv

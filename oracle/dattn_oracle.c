@@ -342,6 +342,7 @@ typedef struct {
     double* out;
     double* m_out;
     double* e_out;
+    const unsigned char* sel; /* [B][Hkv]: compute only selected (b, kv head) items; NULL = all */
     int next; /* atomic work counter over (b, kv head) */
 } batch_job;
 
@@ -355,6 +356,7 @@ static void* batch_worker(void* arg) {
         const int w = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
         if (w >= J->B * J->Hkv) break;
         const int b = w / J->Hkv, kvh = w % J->Hkv;
+        if (J->sel && !J->sel[w]) continue;
         const int64_t lo = J->lo[b], n = J->hi[b] - J->lo[b];
         double* k = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1) * d);
         double* v = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1) * d);
@@ -409,8 +411,20 @@ int or_decode_ranges(uint64_t seed, int B, const int64_t* tok_lo, const int64_t*
                      const uint32_t* seq_ids, int Hq, int Hkv, int d, double scale,
                      int dtype, float amp_q, float amp_k, float amp_v,
                      int threads, double* out, double* m_out, double* e_out) {
+    return or_decode_ranges_sel(seed, B, tok_lo, tok_hi, seq_ids, Hq, Hkv, d, scale, dtype, amp_q,
+                                amp_k, amp_v, NULL, threads, out, m_out, e_out);
+}
+
+/* As or_decode_ranges, computing only the (request, kv head) pairs with
+ * sel[b * Hkv + kvh] != 0 (all q heads of the group); the other outputs are
+ * left untouched. For sampled parity checks of large workloads. */
+int or_decode_ranges_sel(uint64_t seed, int B, const int64_t* tok_lo, const int64_t* tok_hi,
+                         const uint32_t* seq_ids, int Hq, int Hkv, int d, double scale,
+                         int dtype, float amp_q, float amp_k, float amp_v,
+                         const unsigned char* sel, int threads, double* out, double* m_out,
+                         double* e_out) {
     batch_job J = {seed, B, Hq, Hkv, d, dtype, tok_lo, tok_hi, seq_ids, scale,
-                   amp_q, amp_k, amp_v, 0, out, m_out, e_out, 0};
+                   amp_q, amp_k, amp_v, 0, out, m_out, e_out, sel, 0};
     return run_batch(&J, threads);
 }
 
@@ -420,7 +434,7 @@ int or_decode_batch(uint64_t seed, int B, const int64_t* lens, const uint32_t* s
                     int64_t seg_tokens, int threads, double* out) {
     int64_t* lo = (int64_t*)calloc((size_t)B, sizeof(int64_t));
     batch_job J = {seed, B, Hq, Hkv, d, dtype, lo, lens, seq_ids, scale,
-                   amp_q, amp_k, amp_v, seg_tokens, out, NULL, NULL, 0};
+                   amp_q, amp_k, amp_v, seg_tokens, out, NULL, NULL, NULL, 0};
     run_batch(&J, threads);
     free(lo);
     return 0;

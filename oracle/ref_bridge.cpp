@@ -8,9 +8,15 @@
 // path for bench.py --impl reference / cpu_baseline and (3) check that a
 // ctx_rate_curve measured on the B200 (tools/calibrate_ctx_curve.py, SURVEY
 // §8f row 4) is accepted by the reference's own config parser and perf model
-// (perfmodel.cpp, config.cpp).
+// (perfmodel.cpp, config.cpp), (4) pin the GPU store's page ledger to the
+// reference's RManager and blocks_for_tokens (controlplane.cpp:38-79,
+// perfmodel.cpp:178-182) and (5) produce config 5's placement with the
+// reference's own dispatch + rManager heartbeats + gManager plan_round +
+// execute_move_sync (simengine.cpp:252-257, controlplane.cpp:412-485,
+// scheduler.cpp:483-493, controlplane.cpp:518-540).
 #include "kvsched/common.hpp"
 #include "kvsched/config.hpp"
+#include "kvsched/controlplane.hpp"
 #include "kvsched/distattention.hpp"
 #include "kvsched/perfmodel.hpp"
 #include "kvsched/trace.hpp"
@@ -21,6 +27,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -268,6 +275,142 @@ int ref_config_eval(const char* text, int n_x, const double* x, double* g_out, i
         load.ctx_lengths.assign(ctx_lengths, ctx_lengths + batch);
         *layer_time_out = perf::layer_time(load, c.shape, c.f, c.g);
         *n_layers_out = c.shape.n_layers;
+    });
+}
+
+// perf::blocks_for_tokens (perfmodel.cpp:178-182) for a shape with the given
+// block size (every other shape field is set to a valid dummy).
+int ref_blocks_for_tokens(int64_t tokens, int block_size_tokens, int64_t* out) {
+    return guarded([&] {
+        perf::ModelShape shape;
+        shape.n_layers = 1;
+        shape.workload_per_token = 1.0;
+        shape.attn_work_per_ctx_token = 1.0;
+        shape.kv_bytes_per_token = 1.0;
+        shape.block_size_tokens = block_size_tokens;
+        *out = perf::blocks_for_tokens(tokens, shape);
+    });
+}
+
+// Drive one RManager (controlplane.cpp:38-79) through a ledger trace.
+// op[i]: 0 alloc_local(req[i], n[i]), 1 alloc_hosted(req[i], home = n2[i], n[i]),
+// 2 free_request(req[i]). Per op: result[i] = 1/0 for the allocations, the
+// freed block count for free_request; used[i], free_[i] after the op and
+// local[i] = local_blocks(req[i]).
+int ref_rmanager_trace(int64_t capacity, int n_ops, const int* op, const int64_t* req, const int64_t* n,
+                       const int* n2, int64_t* result, int64_t* used, int64_t* free_, int64_t* local) {
+    return guarded([&] {
+        ctrl::RManager rm(0, capacity);
+        for (int i = 0; i < n_ops; ++i) {
+            if (op[i] == 0)
+                result[i] = rm.alloc_local(req[i], n[i]) ? 1 : 0;
+            else if (op[i] == 1)
+                result[i] = rm.alloc_hosted(req[i], n2[i], n[i]) ? 1 : 0;
+            else
+                result[i] = rm.free_request(req[i]);
+            used[i] = rm.used_blocks();
+            free_[i] = rm.free_blocks();
+            local[i] = rm.local_blocks(req[i]);
+        }
+    });
+}
+
+// Config-5 placement from the reference control plane itself:
+//  1. dispatch: requests in order, each homed on the instance with the most
+//     free blocks, ties to the lowest id (simengine.cpp:252-257), blocks via
+//     RManager::alloc_local (controlplane.cpp:38-44);
+//  2. rManager heartbeats -> GManager (epoch recovery, then heartbeats carrying
+//     batch = home requests and the debtor queue `queued` at the home of
+//     request 0), controlplane.cpp:109-142, 374-410, 500-516;
+//  3. `rounds` planning rounds: GManager::plan (snapshots + plan_round,
+//     controlplane.cpp:412-485) and every MoveKvCache executed with
+//     execute_move_sync (controlplane.cpp:518-540); between rounds the freed
+//     blocks admit queued requests of expected_new_request_tokens each
+//     (derive_feasible_batch's rule, scheduler.cpp:62-80), which take their
+//     prompt blocks at the home, and `now` advances by the planning period
+//     (config.hpp:29-39).
+// Model: default_cluster_config(n_inst, capacity) (config.cpp:71-87) and the
+// default SchedulerConfig (scheduler.hpp:52-58).
+// Outputs: home[n_req]; blocks[n_req * n_inst] = blocks of request r held on
+// instance i (local on the home, hosted elsewhere); moves[k*6 .. +5] =
+// (round, req, src, dst, planned blocks, moved blocks) and gains[k], k <
+// max_moves; *n_moves.
+int ref_cfg5_place(int n_inst, int64_t capacity, int64_t queued, int rounds, int n_req,
+                   const int64_t* tokens, int* home, int64_t* blocks, int max_moves, int64_t* moves,
+                   double* gains, int* n_moves) {
+    return guarded([&] {
+        const sim::ClusterConfig cc = sim::default_cluster_config(n_inst, capacity);
+        const int bs = cc.shape.block_size_tokens;
+        std::vector<std::unique_ptr<ctrl::RManager>> rms;
+        std::vector<ctrl::RManager*> raw;
+        for (int i = 0; i < n_inst; ++i) {
+            rms.push_back(std::make_unique<ctrl::RManager>(i, capacity));
+            raw.push_back(rms.back().get());
+        }
+        std::vector<int64_t> batch(n_inst, 0);
+        for (int r = 0; r < n_req; ++r) {
+            int best = 0;
+            for (int i = 1; i < n_inst; ++i)
+                if (rms[i]->free_blocks() > rms[best]->free_blocks()) best = i;
+            const int64_t need = perf::blocks_for_tokens(tokens[r], cc.shape);
+            if (!rms[best]->alloc_local(r, need)) throw ContractError("request does not fit its dispatch target");
+            home[r] = best;
+            batch[best]++;
+        }
+        const int debtor = n_req > 0 ? home[0] : 0;
+        int64_t next_req = n_req;  // ids of admitted (queued) requests
+        ctrl::GManager gm(1);
+        double now = 0.0;
+        ctrl::gmanager_epoch_recover(gm, raw, now);
+        auto heartbeat_all = [&](int64_t q) {
+            for (int i = 0; i < n_inst; ++i) {
+                ctrl::Envelope hb = rms[i]->make_heartbeat(now, batch[i], i == debtor ? q : 0);
+                ctrl::Envelope ack = gm.on_heartbeat(std::get<ctrl::Heartbeat>(hb.msg), now);
+                rms[i]->on_message(ack, now);
+            }
+        };
+        heartbeat_all(queued);
+        const sched::ModelCtx ctx{cc.shape, cc.f, cc.g};
+        int k = 0;
+        for (int round = 0; round < rounds; ++round) {
+            auto out = gm.plan(now, cc.sched, ctx);
+            std::vector<sched::MoveDirective> all = out.plan.reclaims;
+            all.insert(all.end(), out.plan.moves.begin(), out.plan.moves.end());
+            int64_t freed_at_debtor = 0;
+            for (const auto& d : all) {
+                const ctrl::MoveKvCache mv{d.req_id, d.num_blocks, d.dst_instance};
+                const ctrl::MoveResult res =
+                    ctrl::execute_move_sync(*rms[d.src_instance], *rms[d.dst_instance], mv, now, bs);
+                if (d.src_instance == debtor) freed_at_debtor += res.moved_blocks;
+                if (k < max_moves) {
+                    int64_t* m = moves + 6 * k;
+                    m[0] = round; m[1] = d.req_id; m[2] = d.src_instance; m[3] = d.dst_instance;
+                    m[4] = d.num_blocks; m[5] = res.moved_blocks;
+                    gains[k] = d.est_gain;
+                }
+                ++k;
+            }
+            // the freed blocks admit queued requests (derive_feasible_batch,
+            // scheduler.cpp:62-80); they take their prompt blocks at the home
+            // (try_admit, simengine.cpp:262-268), so the next round's reclaim
+            // pass finds no free space to pull the lent blocks back into
+            const int64_t admit = std::min<int64_t>(
+                queued, (freed_at_debtor * bs) / cc.sched.expected_new_request_tokens);
+            const int64_t prompt = perf::blocks_for_tokens(cc.sched.expected_new_request_tokens, cc.shape);
+            for (int64_t a = 0; a < admit; ++a) {
+                if (!rms[debtor]->alloc_local(next_req, prompt)) break;
+                ++next_req;
+                ++batch[debtor];
+                --queued;
+            }
+            now += cc.ctrl.planning_period_s;
+            heartbeat_all(queued);
+        }
+        *n_moves = k;
+        for (int r = 0; r < n_req; ++r)
+            for (int i = 0; i < n_inst; ++i)
+                blocks[static_cast<size_t>(r) * n_inst + i] =
+                    i == home[r] ? rms[i]->local_blocks(r) : rms[i]->hosted_blocks(r, home[r]);
     });
 }
 

@@ -2,8 +2,11 @@
 
 Python host mirror of the C ABI in ``include/dattn.h`` (ctypes, no torch types
 in the boundary). The compute runs in ``_lib/libdattn.so`` (sm_100a kernels);
-there is no CPU fallback: importing this package without the built library
-raises ``ImportError``.
+there is no CPU fallback. The library is mapped on first use (``lib``,
+``Store``, ``comm_unique_id``, ...), so the pure host modules ``workloads`` and
+``sharding`` import without it (bench.py's reference arm must not map the
+product library); any GPU-path call without the built library raises
+``ImportError``.
 
 Reference interface mirrored: ``kvsched::attn`` (proj/include/kvsched/
 distattention.hpp:16-95) and the C ABI conventions of proj/include/kvsched.h
@@ -130,6 +133,9 @@ _FUNCS = {
                                      ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "dattn_kv_append": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_int]),
+    "dattn_kv_synthetic_rows": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_uint64, ctypes.c_float, ctypes.c_float, ctypes.c_void_p,
+                                               ctypes.c_void_p]),
     "dattn_kv_fill_synthetic": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
                                                ctypes.c_uint32, ctypes.c_int64, ctypes.c_float,
                                                ctypes.c_float]),
@@ -143,6 +149,9 @@ _FUNCS = {
                                             ctypes.c_void_p, ctypes.c_void_p]),
     "dattn_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "dattn_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "dattn_comm_abort": (ctypes.c_int, [ctypes.c_void_p]),
+    "dattn_comm_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                       ctypes.POINTER(ctypes.c_int)]),
     "dattn_decode_sharded": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Batch), ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_int]),
     "dattn_kv_send": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
@@ -173,7 +182,21 @@ def _load():
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """ctypes handle of libdattn.so, loaded on first attribute access."""
+    _h = None
+
+    def __getattr__(self, name):
+        if _LazyLib._h is None:
+            _LazyLib._h = _load()
+        return getattr(_LazyLib._h, name)
+
+    @staticmethod
+    def loaded() -> bool:
+        return _LazyLib._h is not None
+
+
+lib = _LazyLib()
 
 
 def last_error() -> str:
@@ -384,6 +407,16 @@ class Store:
         check(lib.dattn_kv_append(self._h, len(seqs), ctypes.cast(arr, ctypes.c_void_p), ptr(k_new),
                                   ptr(v_new), mem))
 
+    def synthetic_rows(self, logical_seqs: Sequence[int], logical_toks: Sequence[int], seed: int, k_dev, v_dev,
+                       amp_k: float = 1.0, amp_v: float = 2.0):
+        """K4's values of (logical_seqs[i], logical_toks[i]) as append rows
+        [n][num_kv_heads][padded_dim] into device buffers."""
+        n = len(logical_seqs)
+        ls = (ctypes.c_uint32 * max(n, 1))(*logical_seqs)
+        lt = (ctypes.c_int64 * max(n, 1))(*logical_toks)
+        check(lib.dattn_kv_synthetic_rows(self._h, n, ctypes.cast(ls, ctypes.c_void_p), ctypes.cast(lt, ctypes.c_void_p),
+                                          seed, amp_k, amp_v, ptr(k_dev), ptr(v_dev)))
+
     def fill_synthetic(self, seq: int, seed: int, logical_seq: int, logical_tok0: int = 0,
                        amp_k: float = 1.0, amp_v: float = 2.0):
         check(lib.dattn_kv_fill_synthetic(self._h, seq, seed, logical_seq, logical_tok0, amp_k, amp_v))
@@ -411,6 +444,17 @@ class Store:
     def comm_init(self, unique_id: bytes, rank: int, nranks: int):
         buf = ctypes.create_string_buffer(unique_id, 128)
         check(lib.dattn_comm_init(self._h, buf, rank, nranks))
+
+    def comm_abort(self):
+        """Make this rank's pending exchange polls give up (dattn_comm_abort)."""
+        check(lib.dattn_comm_abort(self._h))
+
+    def comm_info(self):
+        """(rank, nranks, exchange) as NCCL reports the communicator; exchange
+        1 = ncclAllGather + K3, 2 = K5 NVLink, 3 = MA-kernel push + K6."""
+        r, n, x = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib.dattn_comm_info(self._h, ctypes.byref(r), ctypes.byref(n), ctypes.byref(x)))
+        return r.value, n.value, x.value
 
     def decode_sharded(self, ranges: Sequence[Range], num_rows: int, q, out, mem: int = MEM_DEVICE,
                        chunk_tokens: int = 0, scale: float = 0.0):

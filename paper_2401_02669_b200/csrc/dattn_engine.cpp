@@ -117,6 +117,24 @@ void dattn_store::setup_exchange() {
     // step ahead never writes into the half a slower peer still reads
     xhalf = static_cast<size_t>(nranks) * slot_stride * rec_bytes();
     const size_t xbytes = 2 * xhalf;
+    // poll control: device abort / status words, host-mapped status copy, timeout
+    if (!x_status_host)
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&x_status_host), 64, cudaHostAllocMapped), "cudaHostAlloc");
+    if (!x_ctl_dev) cuda_check(cudaMalloc(&x_ctl_dev, 64), "cudaMalloc(exchange control)");
+    if (!abort_stream)
+        cuda_check(cudaStreamCreateWithFlags(&abort_stream, cudaStreamNonBlocking), "cudaStreamCreate(abort)");
+    cuda_check(cudaMemsetAsync(x_ctl_dev, 0, 64, stream), "cudaMemset(exchange control)");
+    *reinterpret_cast<volatile int*>(x_status_host) = 0;
+    const char* tenv = std::getenv("DATTN_EXCHANGE_TIMEOUT_S");
+    const double tsec = tenv ? std::atof(tenv) : 60.0;
+    x_timeout_ns = static_cast<unsigned long long>((tsec > 0 ? tsec : 60.0) * 1e9);
+    // every CTA of K5 / K6 must be resident at once (their polls wait on
+    // records other CTAs of the same grid push): cap the grid at occupancy
+    for (int kind = 0; kind < 2; ++kind) {
+        int occ = 0;
+        cuda_check(exchange_occupancy(cfg.dtype, dp, kind, &occ), "occupancy(exchange)");
+        x_grid_cap[kind] = std::max(1, std::min(occ * num_sms, kMaxExchangeGrid));
+    }
     cuda_check(cudaMalloc(&xbuf, xbytes), "cudaMalloc(exchange)");
     // every exchange word starts empty (all ones, see XWord in dattn_merge.cuh)
     cuda_check(cudaMemsetAsync(xbuf, 0xFF, xbytes, stream), "cudaMemset(exchange)");
@@ -152,6 +170,18 @@ void dattn_store::setup_exchange() {
     fused_merge = true;
 }
 
+// A poll of an earlier step gave up (abort word or timeout): that step's
+// output is invalid and the exchange words are in an unknown state.
+void dattn_store::check_exchange_status() const {
+    if (!x_status_host) return;
+    const int st = *reinterpret_cast<const volatile int*>(x_status_host);
+    if (st == kXAbortHost)
+        throw Error(DATTN_ERR_NCCL, "NVLink exchange aborted by dattn_comm_abort; call dattn_comm_init to rebuild it");
+    if (st == kXTimeout)
+        throw Error(DATTN_ERR_NCCL, "NVLink exchange: a peer's record did not arrive within DATTN_EXCHANGE_TIMEOUT_S "
+                                    "(a rank failed or stalled); call dattn_comm_init to rebuild the exchange");
+}
+
 dattn_store::~dattn_store() {
     if (k5_trace.p) {
         // DATTN_K5_TRACE summary over all calls: per-CTA mean phase-A and total
@@ -177,6 +207,9 @@ dattn_store::~dattn_store() {
         }
     }
     release_exchange();
+    if (x_status_host) cudaFreeHost(x_status_host);
+    if (x_ctl_dev) cudaFree(x_ctl_dev);
+    if (abort_stream) cudaStreamDestroy(abort_stream);
     if (comm) ncclCommDestroy(comm);
     for (auto& e : comm_ev)
         if (e) cudaEventDestroy(e);
@@ -192,6 +225,7 @@ dattn_store::~dattn_store() {
     if (d_counter) cudaFree(d_counter);
     if (d_flag) cudaFree(d_flag);
     if (meta_ev) cudaEventDestroy(meta_ev);
+    if (app_ev) cudaEventDestroy(app_ev);
     if (own_stream) cudaStreamDestroy(own_stream);
 }
 
@@ -230,6 +264,7 @@ void dattn_store::init(const dattn_store_config& c) {
     cuda_check(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     stream = own_stream;
     cuda_check(cudaEventCreateWithFlags(&meta_ev, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&app_ev, cudaEventDisableTiming), "cudaEventCreate");
     int dev = c.device;
     cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev),
                "cudaDeviceGetAttribute");
@@ -756,6 +791,7 @@ void dattn_store::micro_attention(const dattn_batch& b, const void* q_dev, void*
 
 void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out, int mem) {
     if (!comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
+    check_exchange_status();
     activate();
     Plan& pl = cache_plan;
     plan(b, false, pl);
@@ -798,9 +834,10 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         rp.nranks = nranks;
         rp.slot_stride = slot_stride;
         rp.out_norm = out_dev0;
-        // all CTAs co-resident (<= 4 per SM): identity pushes precede every wait
+        rp.ctl = xctl();
+        // all CTAs co-resident (occupancy cap): identity pushes precede every wait
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8, static_cast<int64_t>(num_sms) * 4)));
+            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + 7) / 8, x_grid_cap[1])));
         cudaEvent_t* ev = timing ? timer_pair(2) : nullptr;
         if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
         cuda_check(launch_rank_merge(cfg.dtype, dp, rp, grid, stream), "launch(K6 rank_merge)");
@@ -811,6 +848,7 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
             cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost, stream),
                        "cudaMemcpyAsync(out)");
             cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+            check_exchange_status();
         }
         return;
     }
@@ -834,14 +872,14 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
         xp.slot_stride = slot_stride;
         xp.out_norm = out_dev0;
         // groups per CTA sweep: 8 (one per warp) when groups are plentiful,
-        // else 1 so a few long groups each get a whole CTA. The grid stays
-        // co-resident (<= 4 CTAs per SM): warps polling in phase D never wait
-        // for a CTA that is not running.
+        // else 1 so a few long groups each get a whole CTA. The grid is capped
+        // at the kernel's occupancy x SMs, so it is co-resident: warps polling
+        // in phase D never wait for a CTA that is not running.
         const int64_t gpc = static_cast<int64_t>(row_recs) >= 1024 ? 8 : 1;
         xp.groups_per_cta = static_cast<int32_t>(gpc);
+        xp.ctl = xctl();
         const int grid = static_cast<int>(std::max<int64_t>(
-            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc,
-                                 std::min<int64_t>(static_cast<int64_t>(num_sms) * 4, kMaxExchangeGrid))));
+            1, std::min<int64_t>((static_cast<int64_t>(row_recs) + gpc - 1) / gpc, x_grid_cap[0])));
         static const bool trace = std::getenv("DATTN_K5_TRACE") != nullptr;
         if (trace) {
             if (!k5_trace.p) {
@@ -861,6 +899,7 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
             cuda_check(cudaMemcpyAsync(out, obuf.p, q_bytes(b.num_rows), cudaMemcpyDeviceToHost, stream),
                        "cudaMemcpyAsync(out)");
             cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+            check_exchange_status();
         }
         return;
     }
@@ -1013,6 +1052,7 @@ dattn_status dattn_store_synchronize(dattn_store* s) {
         REQUIRE_ARG(s, "null store");
         s->activate();
         cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+        s->check_exchange_status();
     });
 }
 
@@ -1147,34 +1187,47 @@ dattn_status dattn_kv_append(dattn_store* s, int n, const int32_t* seqs, const v
         REQUIRE_ARG(seqs && k_new && v_new, "null argument");
         REQUIRE_ARG(mem == DATTN_MEM_DEVICE || mem == DATTN_MEM_HOST, "bad mem kind");
         for (int i = 0; i < n; ++i) s->check_seq(seqs[i]);
-        for (int i = 0; i < n; ++i)
-            for (int j = 0; j < i; ++j)
-                if (seqs[i] == seqs[j]) throw Error(DATTN_ERR_CONTRACT, "duplicate sequence in append");
+        {
+            std::vector<int32_t> sorted(seqs, seqs + n);
+            std::sort(sorted.begin(), sorted.end());
+            if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+                throw Error(DATTN_ERR_CONTRACT, "duplicate sequence in append");
+        }
+        // every page the batch needs must be available before any sequence
+        // grows, so a CAPACITY failure leaves the ledger unchanged
+        int64_t need = 0;
+        for (int i = 0; i < n; ++i) {
+            const int64_t t = s->seq_tokens[seqs[i]];
+            const int64_t pages = (t + 1 + s->cfg.page_tokens - 1) / s->cfg.page_tokens;
+            if (pages > s->cfg.max_pages_per_seq) throw Error(DATTN_ERR_CAPACITY, "sequence exceeds max_pages_per_seq");
+            need += pages - s->seq_pages[seqs[i]];
+        }
+        if (need > static_cast<int64_t>(s->free_pages.size())) throw Error(DATTN_ERR_CAPACITY, "page pool exhausted");
         s->activate();
-        std::vector<int32_t> meta(2 * static_cast<size_t>(n));
+        // the previous append's H2D copy must have consumed the pinned staging
+        cuda_check(cudaEventSynchronize(s->app_ev), "cudaEventSynchronize");
+        const size_t mbytes = 2 * static_cast<size_t>(n) * sizeof(int32_t);
+        s->app_hmeta.ensure(mbytes);
+        s->app_meta.ensure(mbytes);
+        int32_t* meta = static_cast<int32_t*>(s->app_hmeta.p);
         for (int i = 0; i < n; ++i) {
             const int64_t t = s->seq_tokens[seqs[i]];
             s->grow(seqs[i], t + 1);
             meta[i] = seqs[i];
             meta[n + i] = static_cast<int32_t>(t);
         }
+        cuda_check(cudaMemcpyAsync(s->app_meta.p, meta, mbytes, cudaMemcpyHostToDevice, s->stream), "cudaMemcpyAsync");
         const size_t rows = static_cast<size_t>(n) * s->cfg.num_kv_heads * s->dp * s->esz;
-        DevBuf tmp;
-        tmp.ensure(meta.size() * sizeof(int32_t));
-        cuda_check(cudaMemcpyAsync(tmp.p, meta.data(), meta.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
-                                   s->stream),
-                   "cudaMemcpyAsync");
         const void* kd = k_new;
         const void* vd = v_new;
-        DevBuf rowsbuf;
         if (mem == DATTN_MEM_HOST) {
-            rowsbuf.ensure(2 * rows);
-            cuda_check(cudaMemcpyAsync(rowsbuf.p, k_new, rows, cudaMemcpyHostToDevice, s->stream), "cudaMemcpyAsync");
-            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(rowsbuf.p) + rows, v_new, rows, cudaMemcpyHostToDevice,
+            s->app_rows.ensure(2 * rows);
+            cuda_check(cudaMemcpyAsync(s->app_rows.p, k_new, rows, cudaMemcpyHostToDevice, s->stream), "cudaMemcpyAsync");
+            cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(s->app_rows.p) + rows, v_new, rows, cudaMemcpyHostToDevice,
                                        s->stream),
                        "cudaMemcpyAsync");
-            kd = rowsbuf.p;
-            vd = static_cast<uint8_t*>(rowsbuf.p) + rows;
+            kd = s->app_rows.p;
+            vd = static_cast<uint8_t*>(s->app_rows.p) + rows;
         }
         AppendParams p{};
         p.k_pool = s->kpool;
@@ -1183,14 +1236,48 @@ dattn_status dattn_kv_append(dattn_store* s, int n, const int32_t* seqs, const v
         p.bt_stride = s->cfg.max_pages_per_seq;
         p.page_tokens = s->cfg.page_tokens;
         p.num_kv_heads = s->cfg.num_kv_heads;
-        p.seqs = static_cast<const int32_t*>(tmp.p);
-        p.positions = static_cast<const int32_t*>(tmp.p) + n;
+        p.seqs = static_cast<const int32_t*>(s->app_meta.p);
+        p.positions = static_cast<const int32_t*>(s->app_meta.p) + n;
         p.k_new = kd;
         p.v_new = vd;
         p.n = n;
         cuda_check(launch_append(s->cfg.dtype, s->dp, p, s->stream), "launch(append)");
+        cuda_check(cudaEventRecord(s->app_ev, s->stream), "cudaEventRecord");
         count_launch(1);
-        // the temporaries are freed on return: finish before that
+    });
+}
+
+dattn_status dattn_kv_synthetic_rows(dattn_store* s, int n, const uint32_t* logical_seqs,
+                                     const int64_t* logical_toks, uint64_t seed, float amp_k, float amp_v,
+                                     void* k_dev, void* v_dev) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        if (n <= 0) return;
+        REQUIRE_ARG(logical_seqs && logical_toks && k_dev && v_dev, "null argument");
+        for (int i = 0; i < n; ++i)
+            if (logical_toks[i] < 0) throw Error(DATTN_ERR_CONTRACT, "negative token index");
+        s->activate();
+        const size_t bytes = static_cast<size_t>(n) * (sizeof(uint32_t) + sizeof(int64_t));
+        DevBuf tmp;
+        tmp.ensure(bytes);
+        std::vector<unsigned char> h(bytes);
+        std::memcpy(h.data(), logical_toks, n * sizeof(int64_t));
+        std::memcpy(h.data() + n * sizeof(int64_t), logical_seqs, n * sizeof(uint32_t));
+        cuda_check(cudaMemcpyAsync(tmp.p, h.data(), bytes, cudaMemcpyHostToDevice, s->stream), "cudaMemcpyAsync");
+        RowsSynthParams p{};
+        p.k_out = k_dev;
+        p.v_out = v_dev;
+        p.logical_tok = static_cast<const int64_t*>(tmp.p);
+        p.logical_seq = reinterpret_cast<const uint32_t*>(static_cast<unsigned char*>(tmp.p) + n * sizeof(int64_t));
+        p.n = n;
+        p.num_kv_heads = s->cfg.num_kv_heads;
+        p.head_dim = s->cfg.head_dim;
+        p.seed = seed;
+        p.amp_k = amp_k;
+        p.amp_v = amp_v;
+        cuda_check(launch_rows_synth(s->cfg.dtype, s->dp, p, s->stream), "launch(rows_synth)");
+        count_launch(1);
+        // tmp is freed on return
         cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
     });
 }
@@ -1292,12 +1379,46 @@ dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE
         s->activate();
         ncclUniqueId u;
         std::memcpy(&u, id, sizeof(u));
+        // unmap the previous world's peer buffers while rank / nranks still
+        // describe it (release_exchange skips the old own rank)
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+        s->release_exchange();
         if (s->comm) ncclCommDestroy(s->comm);
         s->comm = nullptr;
+        s->rank = 0;
+        s->nranks = 1;
         nccl_check(ncclCommInitRank(&s->comm, nranks, u, rank), "ncclCommInitRank");
         s->rank = rank;
         s->nranks = nranks;
         if (nranks > 1) s->setup_exchange();
+    });
+}
+
+dattn_status dattn_comm_abort(dattn_store* s) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        if (!s->x_ctl_dev) return;
+        // the abort word lives in device memory: write it from a stream that
+        // runs beside the exchange kernel the polls are in
+        static const int one = 1;
+        cuda_check(cudaSetDevice(s->cfg.device), "cudaSetDevice");
+        cuda_check(cudaMemcpyAsync(s->x_ctl_dev, &one, sizeof(int), cudaMemcpyHostToDevice, s->abort_stream),
+                   "cudaMemcpyAsync(abort)");
+        cuda_check(cudaStreamSynchronize(s->abort_stream), "cudaStreamSynchronize(abort)");
+    });
+}
+
+dattn_status dattn_comm_info(const dattn_store* s, int* rank, int* nranks, int* exchange) {
+    return guarded([&] {
+        REQUIRE_ARG(s && rank && nranks && exchange, "null argument");
+        if (!s->comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
+        int r = -1, n = -1;
+        nccl_check(ncclCommUserRank(s->comm, &r), "ncclCommUserRank");
+        nccl_check(ncclCommCount(s->comm, &n), "ncclCommCount");
+        const char* k1 = std::getenv("DATTN_FUSED_K1");
+        *rank = r;
+        *nranks = n;
+        *exchange = !s->fused_merge ? 1 : (k1 && std::atoi(k1) == 1 ? 3 : 2);
     });
 }
 

@@ -84,6 +84,11 @@ struct dattn_store {
     int64_t used_pages = 0;
 
     dattn::DevBuf d_meta, recs, rowrecs, qbuf, obuf, gathered, d_staging;
+    // kv_append: persistent staging (the call is asynchronous on the store
+    // stream); app_ev guards the pinned meta staging against reuse
+    dattn::DevBuf app_meta, app_rows;
+    dattn::HostBuf app_hmeta;
+    cudaEvent_t app_ev = nullptr;
     dattn::HostBuf h_meta, h_staging;
     size_t staging_used = 0;
     unsigned long long work_base = 0;
@@ -111,6 +116,15 @@ struct dattn_store {
     }
     uint32_t epoch = 0;  // step counter: its parity selects the half
     bool fused_merge = false;
+    // poll control (dattn_internal.h XCtl): device [0] abort, [1] status;
+    // host-mapped status copy; the abort word is written on abort_stream
+    int* x_ctl_dev = nullptr;
+    int* x_status_host = nullptr;
+    cudaStream_t abort_stream = nullptr;
+    unsigned long long x_timeout_ns = 0;
+    int x_grid_cap[2] = {0, 0};  // co-resident CTAs of K5, K6 (occupancy x SMs)
+    dattn::XCtl xctl() const { return {x_timeout_ns, x_ctl_dev, x_ctl_dev + 1, x_status_host}; }
+    void check_exchange_status() const;
     void setup_exchange();
     void release_exchange();
 

@@ -58,6 +58,27 @@ struct MAParams {
     int64_t slot_stride;             // records per source rank
 };
 
+// Failure control of the NVLink exchange polls (K5 phase D, K6). A poll that
+// has waited for more than kXSlowNs checks, every 256 spins, the abort word
+// (device memory, set by dattn_comm_abort through a copy on another stream)
+// and its own timeout. On abort or after timeout_ns it records the reason in
+// *status_dev (so every other waiting poll of the launch returns at once) and
+// in *status_host (host-mapped, read by the engine without a sync) and
+// returns instead of trapping: the CUDA context survives a peer that never
+// arrives (a rank that failed before launching, a host stalled past the
+// timeout). The step's output is then invalid and the engine refuses further
+// exchanges until dattn_comm_init rebuilds the buffers. The fast path (data
+// arrives within kXSlowNs) touches no control word; the kernel never reads
+// host memory.
+constexpr int kXAbortHost = 1, kXTimeout = 2;
+constexpr unsigned long long kXSlowNs = 20000;
+struct XCtl {
+    unsigned long long timeout_ns;
+    const int* abort_dev;  // device word; nonzero -> give up
+    int* status_dev;       // device word; 0 ok, else kXAbortHost / kXTimeout
+    int* status_host;      // host-mapped copy of the reason (written on failure only)
+};
+
 // K6: rank merge after fused K1/K2 (waits until every rank delivered all groups).
 struct RankMergeParams {
     int32_t rows;
@@ -70,6 +91,7 @@ struct RankMergeParams {
     int32_t nranks;
     int64_t slot_stride;
     void* out_norm;
+    XCtl ctl;
 };
 
 // K3 merge launch.
@@ -99,6 +121,7 @@ struct XParams {
     int32_t groups_per_cta;            // 8 or 1
     void* out_norm;                    // [rows*heads][DP] storage dtype
     unsigned long long* trace;         // debug (DATTN_K5_TRACE): [kMaxExchangeGrid][3] sums, else null
+    XCtl ctl;
 };
 
 struct FillParams {
@@ -129,6 +152,21 @@ struct AppendParams {
     const void* k_new;         // [n][Hkv][DP]
     const void* v_new;
     int32_t n;
+};
+
+// Synthetic K/V rows [n][Hkv][DP] for logical (sequence, token) pairs: the
+// values K4 would write at those positions (decode-loop inputs).
+struct RowsSynthParams {
+    void* k_out;
+    void* v_out;
+    const uint32_t* logical_seq;  // [n]
+    const int64_t* logical_tok;   // [n]
+    int32_t n;
+    int32_t num_kv_heads;
+    int32_t head_dim;
+    uint64_t seed;
+    float amp_k;
+    float amp_v;
 };
 
 struct QFillParams {
@@ -166,10 +204,14 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
                       cudaStream_t st);
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st);
+// Resident CTAs per SM of K5 (kind 0) / K6 (kind 1): their polls need the
+// whole grid co-resident, so the engine caps the grid at this x num_sms.
+cudaError_t exchange_occupancy(int dtype, int dp, int kind, int* blocks_per_sm);
 cudaError_t launch_rank_merge(int dtype, int dp, const RankMergeParams& p, int grid, cudaStream_t st);
 cudaError_t launch_fill_kv(int dtype, int dp, const FillParams& p, cudaStream_t st);
 cudaError_t launch_append(int dtype, int dp, const AppendParams& p, cudaStream_t st);
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st);
+cudaError_t launch_rows_synth(int dtype, int dp, const RowsSynthParams& p, cudaStream_t st);
 cudaError_t launch_scatter(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
 cudaError_t launch_gather(int dtype, int dp, const ScatterParams& p, cudaStream_t st);
 // K2 (tcgen05 GQA path, dattn_gqa_tc.cu)

@@ -666,7 +666,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
 // Light groups are merged by one warp each, heavy groups by the whole CTA.
 // Identity groups (no tokens on this rank) push only their header; a receiver
 // reads the payload of live records only, so every word written is read and
-// emptied exactly once. The grid is co-resident (<= 4 CTAs per SM), so a warp
+// emptied exactly once. The engine caps the grid at the kernel's occupancy x
+// SMs (exchange_occupancy), so the whole grid is co-resident and a warp
 // spinning in phase D never starves a CTA still in phase A.
 template <typename T, int DP>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const XParams x) {
@@ -936,7 +937,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     U* X = static_cast<U*>(x.peer_x[x.rank]);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
          g += static_cast<int64_t>(gridDim.x) * kMergeWarps)
-        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane);
+        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane, x.ctl);
     __syncthreads();
     stamp(4);
 }
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) rank_merge_kernel(const Rank
     U* X = static_cast<U*>(x.peer_x[x.rank]);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp; g < groups;
          g += static_cast<int64_t>(gridDim.x) * kMergeWarps)
-        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane);
+        xchg_rank_merge<T, DP>(X, g, x.nranks, x.slot_stride, x.out_norm, lane, x.ctl);
 }
 
 // ------------------------------------------------------------------ K4
@@ -1060,6 +1061,29 @@ __global__ void fill_q_kernel(const QFillParams p) {
         const uint32_t row = static_cast<uint32_t>(rh / p.heads) + p.row0;
         q[i] = j < p.head_dim ? store_as<T>(synth_f32(kq, elem_index(row, h, 0, j), p.amp))
                               : store_as<T>(0.f);
+    }
+}
+
+template <typename T, int DP>
+__global__ void rows_synth_kernel(const RowsSynthParams p) {
+    const uint64_t kk = stream_key(p.seed, 1), kv = stream_key(p.seed, 2);
+    const int64_t total = static_cast<int64_t>(p.n) * p.num_kv_heads * DP;
+    T* ko = static_cast<T*>(p.k_out);
+    T* vo = static_cast<T*>(p.v_out);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % DP);
+        const int64_t sh = i / DP;
+        const int h = static_cast<int>(sh % p.num_kv_heads);
+        const int s = static_cast<int>(sh / p.num_kv_heads);
+        if (j < p.head_dim) {
+            const uint64_t ix = elem_index(p.logical_seq[s], h, static_cast<uint32_t>(p.logical_tok[s]), j);
+            ko[i] = store_as<T>(synth_f32(kk, ix, p.amp_k));
+            vo[i] = store_as<T>(synth_f32(kv, ix, p.amp_v));
+        } else {
+            ko[i] = store_as<T>(0.f);
+            vo[i] = store_as<T>(0.f);
+        }
     }
 }
 
@@ -1246,6 +1270,21 @@ cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid,
     return e;
 }
 
+cudaError_t exchange_occupancy(int dtype, int dp, int kind, int* blocks_per_sm) {
+    cudaError_t e = cudaSuccess;
+    *blocks_per_sm = 0;
+    if (kind == 0) {
+        DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                                         blocks_per_sm, merge_exchange_kernel<TC, DPC>,
+                                                         32 * kMergeWarps, 0))));
+    } else {
+        DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                                         blocks_per_sm, rank_merge_kernel<TC, DPC>,
+                                                         32 * kMergeWarps, 0))));
+    }
+    return e;
+}
+
 cudaError_t launch_rank_merge(int dtype, int dp, const RankMergeParams& p, int grid, cudaStream_t st) {
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (rank_merge_kernel<TC, DPC><<<grid, 32 * kMergeWarps, 0, st>>>(p))));
     return cudaGetLastError();
@@ -1266,6 +1305,12 @@ cudaError_t launch_append(int dtype, int dp, const AppendParams& p, cudaStream_t
 cudaError_t launch_fill_q(int dtype, int dp, const QFillParams& p, cudaStream_t st) {
     const int grid = grid_for(static_cast<int64_t>(p.rows) * p.heads * dp);
     DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (fill_q_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_synth(int dtype, int dp, const RowsSynthParams& p, cudaStream_t st) {
+    const int grid = grid_for(static_cast<int64_t>(p.n) * p.num_kv_heads * dp);
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (rows_synth_kernel<TC, DPC><<<grid, 256, 0, st>>>(p))));
     return cudaGetLastError();
 }
 

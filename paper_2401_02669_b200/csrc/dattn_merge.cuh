@@ -141,10 +141,13 @@ __device__ __forceinline__ uint4 ld_volatile_v4(const void* p) {
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
     return v;
 }
-// Spin until none of the N words is empty (bounded: a peer that never
-// delivers traps after 10 s instead of wedging the GPU).
+// Spin until none of the N words is empty. A poll still waiting after
+// kXSlowNs checks the control words every 256 spins: another poll's failure
+// (status), the host's abort word and the timeout; on abort / timeout it
+// records the reason (XCtl) and returns with the words it has (the step's
+// output is invalid, the context stays alive).
 template <class U, int N>
-__device__ __forceinline__ void x_poll(const U* p, U (&w)[N]) {
+__device__ __forceinline__ void x_poll(const U* p, U (&w)[N], const XCtl& ctl) {
     uint64_t t0 = 0;
     for (int spin = 0;; ++spin) {
         bool ok = true;
@@ -161,8 +164,20 @@ __device__ __forceinline__ void x_poll(const U* p, U (&w)[N]) {
         if ((spin & 255) == 0) {
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (spin == 0) t0 = t;
-            else if (t - t0 > 10000000000ull) __trap();
+            if (spin == 0) {
+                t0 = t;
+            } else if (t - t0 > kXSlowNs) {
+                if (*reinterpret_cast<const volatile int*>(ctl.status_dev) != 0) return;
+                int reason = 0;
+                if (*reinterpret_cast<const volatile int*>(ctl.abort_dev) != 0) reason = kXAbortHost;
+                else if (t - t0 > ctl.timeout_ns) reason = kXTimeout;
+                if (reason) {
+                    *reinterpret_cast<volatile int*>(ctl.status_dev) = reason;
+                    *reinterpret_cast<volatile int*>(ctl.status_host) = reason;
+                    __threadfence_system();
+                    return;
+                }
+            }
         }
     }
 }
@@ -377,7 +392,8 @@ __device__ __forceinline__ int32_t mq_pop(MergeQueue* q, int idx) {
 // rank's next-step records). Identity records carry only a header.
 template <typename T, int DP>
 __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>::Acc>::U* X, int64_t g, int nranks,
-                                                int64_t slot_stride, void* out_norm, int lane) {
+                                                int64_t slot_stride, void* out_norm, int lane,
+                                                const XCtl& ctl) {
     using E = Elem<T>;
     using Acc = typename E::Acc;
     using U = typename XWord<Acc>::U;
@@ -398,7 +414,7 @@ __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>:
     Acc mr = kNegInf, er = 0, tr = 0;
     if (lane < nranks) {
         U h[4];
-        x_poll<U, 4>(X + (static_cast<int64_t>(lane) * slot_stride + g) * REC, h);
+        x_poll<U, 4>(X + (static_cast<int64_t>(lane) * slot_stride + g) * REC, h, ctl);
         mr = x_dec<Acc>(h[0]);
         er = x_dec<Acc>(h[1]);
         tr = x_dec<Acc>(h[2]);
@@ -431,7 +447,7 @@ __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>:
                     bool ok = true;
 #pragma unroll
                     for (int v = 0; v < kVW; ++v) ok &= pay[r][v] != ~U(0);
-                    if (!ok) x_poll<U, kVW>(X + (static_cast<int64_t>(r) * slot_stride + g) * REC + 4 + lane * kVW, pay[r]);
+                    if (!ok) x_poll<U, kVW>(X + (static_cast<int64_t>(r) * slot_stride + g) * REC + 4 + lane * kVW, pay[r], ctl);
 #pragma unroll
                     for (int v = 0; v < kVW; ++v) a2[0][v] += x_dec<Acc>(pay[r][v]) * w;
                 }
@@ -452,7 +468,7 @@ __device__ __forceinline__ void xchg_rank_merge(typename XWord<typename Elem<T>:
                 const int j = sw * kPer + lane * kVW;
                 if (j < DP) {
                     U dw[kVW];
-                    x_poll<U, kVW>(rec + 4 + j, dw);
+                    x_poll<U, kVW>(rec + 4 + j, dw, ctl);
 #pragma unroll
                     for (int v = 0; v < kVW; ++v) a2[sw][v] += x_dec<Acc>(dw[v]) * w;
                 }

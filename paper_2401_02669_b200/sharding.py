@@ -13,11 +13,16 @@ Two placements:
     instance) (MoveDirective, proj/include/kvsched/scheduler.hpp:68-75; the
     RManager ledgers controlplane.hpp:212-215) turned into token ranges: the
     home instance keeps the prefix, lenders take consecutive block ranges in
-    ascending instance id (config 5).
+    ascending instance id (config 5). The counts for config 5 are the
+    reference control plane's own output (tests/golden/cfg5_placement.json,
+    made by tests/golden/make_cfg5_placement.py from oracle/_ref), read by
+    ``gmanager_placement``.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
+import json
+import os
 from typing import Dict, List, Sequence, Tuple
 
 
@@ -99,41 +104,26 @@ def coverage_ok(per_rank: List[List[RankRange]], lens: Sequence[int]) -> bool:
     return True
 
 
-def planner_placement(lens: Sequence[int], nranks: int, block_tokens: int,
-                      retain_local_fraction: float = 0.5):
-    """Config-5 placement, the reference policy restated on block counts.
+CFG5_PLACEMENT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                              "cfg5_placement.json")
 
-    1. Dispatch: requests in order, each homed on the instance with the most
-       free blocks, i.e. the least loaded (simengine.cpp:252-257); ties go to
-       the lowest id.
-    2. Lending (gManager plan_round, scheduler.cpp:215-295): an instance above
-       the fair share ceil(total/N) lends blocks of its requests to instances
-       below it, in ascending instance id, but every request keeps at least
-       ceil(retain_local_fraction * blocks) at home (movable_blocks,
-       scheduler.cpp:425-431; retain_local_fraction scheduler.hpp:56).
-    Returns (homes, lent_blocks) for placement_from_moves.
-    """
-    nb = [_blocks(L, block_tokens) for L in lens]
-    load = [0] * nranks
-    homes = []
-    for b in nb:
-        h = min(range(nranks), key=lambda r: (load[r], r))
-        homes.append(h)
-        load[h] += b
-    target = -(-sum(nb) // nranks)
-    lent: Dict[Tuple[int, int], int] = {}
-    for req, b in enumerate(nb):
-        h = homes[req]
-        keep_min = -(-int(retain_local_fraction * b * 1000) // 1000)
-        movable = max(0, min(b - keep_min, load[h] - target))
-        for r in range(nranks):
-            if movable <= 0:
-                break
-            if r == h or load[r] >= target:
-                continue
-            take = min(movable, target - load[r])
-            lent[(req, r)] = lent.get((req, r), 0) + take
-            load[r] += take
-            load[h] -= take
-            movable -= take
-    return homes, lent
+
+def gmanager_placement(lens: Sequence[int], nranks: int, queued: int, block_tokens: int = 16,
+                       path: str = CFG5_PLACEMENT):
+    """Config 5's (homes, lent_blocks) as the reference control plane placed
+    them: dispatch to the most-free instance, heartbeats, GManager::plan +
+    execute_move_sync until no move (see tests/golden/make_cfg5_placement.py).
+    Returns inputs for ``placement_from_moves``. Raises ``ValueError`` when the
+    fixture has no entry for (nranks, queued) or describes other lengths."""
+    with open(path) as f:
+        j = json.load(f)
+    d = j["lens"]
+    if list(lens) != [d["long"]] + [d["short"]] * d["n_short"] or block_tokens != j["block_tokens"]:
+        raise ValueError("the config-5 placement fixture describes another batch")
+    key = f"n{nranks}_q{queued}"
+    if key not in j["placements"]:
+        raise ValueError(f"no reference placement for {nranks} instances and queue {queued} "
+                         f"(have {sorted(j['placements'])})")
+    p = j["placements"][key]
+    lent = {(r, i): b for r, i, b in p["hosted"]}
+    return list(p["homes"]), lent

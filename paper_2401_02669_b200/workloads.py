@@ -44,7 +44,8 @@ class Workload:
     amp_k: float = 1.0
     amp_v: float = 2.0
     note: str = ""
-    placement: str = "equal"  # "equal": plan_rank_ranges; "planner": planner_placement
+    placement: str = "equal"  # "equal": plan_rank_ranges; "gmanager": the reference control plane's placement
+    queued: int = 0  # config 5: debtor queue at the long request's home (gmanager placement input)
     n_layers: int = 32  # model depth for model-equivalent TPS (7B: 32, 70B: 80)
     meta: dict = field(default_factory=dict)
 
@@ -70,8 +71,9 @@ class Workload:
         return 4 * self.hq * self.d * self.total_tokens
 
 
-def config(name: str) -> Workload:
-    """BASELINE.json configs by number (1..5)."""
+def config(name: str, cfg5_queue: int = 64) -> Workload:
+    """BASELINE.json configs by number (1..5). ``cfg5_queue`` selects config 5's
+    reference placement (debtor queue 0, 64 or 512; tests/golden/cfg5_placement.json)."""
     if name in ("1", "cfg1"):
         return Workload("cfg1: 1 req, LLaMA-7B MHA 32x128, 4K fp32 KV in 4 rBlocks", [4096], 32, 32, 128, 1,
                         rblocks=4)
@@ -85,17 +87,19 @@ def config(name: str) -> Workload:
     if name in ("4", "cfg4"):
         return Workload("cfg4: 1 req x 1M tokens, LLaMA-7B MHA 32x128, bf16", [1048576], 32, 32, 128, 0)
     if name in ("5", "cfg5"):
-        return Workload("cfg5: skewed mix 1x512K + 256x2K, LLaMA-7B MHA 32x128, bf16, gManager-policy placement",
-                        [524288] + [2048] * 256, 32, 32, 128, 0, placement="planner",
-                        meta={"placement": "sharding.planner_placement: least-loaded dispatch, lending "
-                                           "above fair share with >=50% of blocks kept home"})
+        return Workload("cfg5: skewed mix 1x512K + 256x2K, LLaMA-7B MHA 32x128, bf16, gManager placement",
+                        [524288] + [2048] * 256, 32, 32, 128, 0, placement="gmanager", queued=cfg5_queue,
+                        meta={"placement": "reference control plane (oracle/_ref): most-free dispatch, "
+                                           "rManager heartbeats, GManager::plan + execute_move_sync until no "
+                                           "move; tests/golden/cfg5_placement.json",
+                              "debtor_queue": cfg5_queue, "capacity_blocks": 32768})
     raise ValueError(f"unknown config {name!r}")
 
 
 def rank_shares(w: Workload, nranks: int):
     """Per-rank token ranges of every request (sharding.RankRange lists)."""
-    from .sharding import placement_from_moves, plan_rank_ranges, planner_placement
-    if w.placement == "planner":
-        homes, lent = planner_placement(w.lens, nranks, w.page_tokens)
+    from .sharding import gmanager_placement, placement_from_moves, plan_rank_ranges
+    if w.placement == "gmanager" and nranks > 1:
+        homes, lent = gmanager_placement(w.lens, nranks, w.queued, w.page_tokens)
         return placement_from_moves(w.lens, homes, lent, nranks, w.page_tokens)
     return plan_rank_ranges(w.lens, nranks, w.page_tokens)

@@ -34,6 +34,9 @@ CASES = {
     "gqa_bf16": dict(lens=[5000, 37, 20000, 1, 16], hq=64, hkv=8, d=128, dtype=0, tol=2e-2),
     "mha_f32": dict(lens=[4096, 3, 777], hq=32, hkv=32, d=128, dtype=1, tol=1e-3),
     "mha_f64": dict(lens=[900, 5, 2000], hq=8, hkv=8, d=64, dtype=2, tol=1e-10),
+    # 257 rows x 32 heads = 8,224 (row, q head) groups: more than the exchange
+    # kernels' co-resident CTAs (K5 / K6 grids are capped at occupancy x SMs)
+    "many_groups_bf16": dict(lens=[3000] + [40] * 256, hq=32, hkv=32, d=128, dtype=0, tol=2e-2),
 }
 
 
@@ -57,9 +60,11 @@ def _worker(rank, world, port, case, placement, fused, q):
         lens, hq, hkv, d, dt = c["lens"], c["hq"], c["hkv"], c["d"], c["dtype"]
         seed = 404
         if placement:
-            nb = -(-lens[2] // 16)
-            lent = {(2, (r + 1) % world): nb // (world + 1) for r in range(world - 1)}
-            shares = placement_from_moves(lens, [0] * len(lens), lent, world, 16)[rank]
+            lr = max(range(len(lens)), key=lambda i: lens[i])  # lend the longest request's tail
+            nb = -(-lens[lr] // 16)
+            lent = {(lr, (r + 1) % world): nb // (world + 1) for r in range(world - 1)}
+            homes = [0 if i == lr else i % world for i in range(len(lens))]
+            shares = placement_from_moves(lens, homes, lent, world, 16)[rank]
         else:
             shares = plan_rank_ranges(lens, world, 16)[rank]
         pages = sum(-(-rr.tokens // 16) for rr in shares) + 8
@@ -150,7 +155,7 @@ def _worker(rank, world, port, case, placement, fused, q):
 @pytest.mark.parametrize("fused", sorted(MODES))
 def test_sharded_decode_matches_oracle(case, placement, fused):
     import torch.multiprocessing as mp
-    world = min(_ngpus(), 4)
+    world = min(_ngpus(), 8)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -230,7 +235,7 @@ def _migrate_worker(rank, world, port, q):
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_kv_block_migration_between_gpus():
     import torch.multiprocessing as mp
-    world = min(_ngpus(), 4)
+    world = min(_ngpus(), 8)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -245,3 +250,100 @@ def test_kv_block_migration_between_gpus():
         assert ok
         if rank == 0:
             assert err < 2e-2, err
+
+
+def _abort_worker(rank, world, port, q):
+    """A rank that never launches its step (it failed before the exchange)
+    must not kill its peers' CUDA contexts: their polls give up after
+    DATTN_EXCHANGE_TIMEOUT_S, the step reports DATTN_ERR_NCCL, and
+    dattn_comm_init rebuilds a working exchange. dattn_comm_abort ends a
+    pending wait at once."""
+    import sys
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_02669_b200 as pb
+    try:
+        os.environ["DATTN_EXCHANGE_TIMEOUT_S"] = "2"
+        os.environ["DATTN_FUSED_MERGE"] = "1"
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        st = pb.Store(128, 8, 8, pb.BF16, 16, 64, max_seqs=4, max_pages_per_seq=32, device=rank)
+        st.set_stream(torch.cuda.current_stream().cuda_stream)
+        s0 = st.seq_create(300)
+        st.fill_synthetic(s0, 9, 0, 300 * rank, 1.0, 2.0)
+        qd = torch.empty(1, 8, 128, dtype=torch.bfloat16, device=f"cuda:{rank}")
+        st.q_fill_synthetic(qd, 1, 9)
+        out = torch.zeros_like(qd)
+        rg = [pb.Range(s0, 0, 0, 300)]
+
+        def init():
+            uid = [pb.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            st.comm_init(uid[0], rank, world)
+
+        init()
+        st.decode_sharded(rg, 1, qd, out)
+        st.synchronize()
+        good = out.clone()
+        res = {}
+        # 1. the last rank skips the step: everyone else times out, no trap
+        dist.barrier()
+        if rank != world - 1:
+            t0 = time.time()
+            st.decode_sharded(rg, 1, qd, out)
+            try:
+                st.synchronize()
+                res["timeout"] = "no error"
+            except pb.DattnError as e:
+                res["timeout"] = e.status == pb.ERR_NCCL and 1.5 < time.time() - t0 < 30
+            try:
+                st.decode_sharded(rg, 1, qd, out)
+                res["refused"] = False
+            except pb.DattnError:
+                res["refused"] = True
+        dist.barrier()
+        # 2. rebuild; a normal step works and reproduces the first result
+        init()
+        st.decode_sharded(rg, 1, qd, out)
+        st.synchronize()
+        res["rebuilt"] = bool(torch.equal(out, good))
+        # 3. dattn_comm_abort ends a wait that would otherwise last 2 s
+        dist.barrier()
+        if rank == 0:
+            t0 = time.time()
+            st.decode_sharded(rg, 1, qd, out)  # peers do not launch
+            time.sleep(0.2)
+            st.comm_abort()
+            try:
+                st.synchronize()
+                res["abort"] = "no error"
+            except pb.DattnError as e:
+                res["abort"] = e.status == pb.ERR_NCCL and time.time() - t0 < 1.5
+        dist.barrier()
+        ok = all(v is True for v in res.values())
+        q.put((rank, ok, None if ok else repr(res)))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, False, repr(e)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_exchange_timeout_and_abort_do_not_trap():
+    import torch.multiprocessing as mp
+    world = min(_ngpus(), 8)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_abort_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, exc in res:
+        assert ok, (rank, exc)

@@ -105,6 +105,74 @@ def test_block_tables_match_ledger(torch_cuda):
         st.seq_tokens(seqs[-1])  # released
 
 
+@pytest.mark.skipif(not __import__("oracle").ref_available(), reason="oracle/_ref not built")
+def test_page_ledger_bit_exact_with_reference_rmanager(torch_cuda):
+    """The store's page ledger against the compiled reference RManager
+    (controlplane.cpp:38-79) and blocks_for_tokens (perfmodel.cpp:178-182): a
+    seeded trace of create / resize / append / release, including pool
+    exhaustion, maps onto alloc_local / free_request. After every operation the
+    used and free page counts, the sequence's page count and the capacity
+    outcome (CapacityError <-> alloc_local returning false) must agree."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    cap, page = 48, 16
+    st = pb.Store(128, 2, 2, pb.BF16, page, cap, max_seqs=64, max_pages_per_seq=cap)
+    st.set_stream(torch.cuda.current_stream().cuda_stream)
+    rng = np.random.default_rng(2024)
+    live = {}  # req -> (seq, tokens)
+    ops, mine = [], []
+    next_req = 0
+    for _ in range(300):
+        kind = rng.integers(0, 4)
+        if kind == 0 or not live:  # create (RManager::alloc_local of the prompt blocks)
+            toks = int(rng.integers(1, 12 * page))
+            need = oracle.ref_blocks_for_tokens(toks, page)
+            try:
+                s = st.seq_create(toks)
+                ok = 1
+                live[next_req] = (s, toks)
+            except pb.CapacityError:
+                ok = 0
+            ops.append((oracle.LEDGER_ALLOC_LOCAL, next_req, need))
+            mine.append((ok, next_req))
+            next_req += 1
+            continue
+        req = int(rng.choice(sorted(live)))
+        s, toks = live[req]
+        if kind in (1, 2):  # resize / append: the next blocks (ensure_slot's local path)
+            new = toks + (1 if kind == 2 else int(rng.integers(1, 5 * page)))
+            need = oracle.ref_blocks_for_tokens(new, page) - oracle.ref_blocks_for_tokens(toks, page)
+            try:
+                if kind == 2:
+                    kn = torch.zeros(1, 2, 128, dtype=torch.bfloat16, device="cuda")
+                    st.kv_append([s], kn, kn)
+                else:
+                    st.seq_resize(s, new)
+                ok = 1
+                live[req] = (s, new)
+            except pb.CapacityError:
+                ok = 0
+            if need == 0:
+                assert ok == 1
+                continue  # no ledger operation (the reference allocates nothing)
+            ops.append((oracle.LEDGER_ALLOC_LOCAL, req, need))
+            mine.append((ok, req))
+        else:  # release
+            freed = st.seq_release(s)
+            del live[req]
+            ops.append((oracle.LEDGER_FREE, req, 0))
+            mine.append((freed, req))
+        ref = oracle.ref_rmanager_trace(cap, ops)[-1]
+        info = st.info()
+        got_local = len(st.block_table(live[req][0])) if req in live else 0
+        assert (mine[-1][0], info.used_pages, info.free_pages, got_local) == ref, (len(ops), ops[-1])
+    ref_all = oracle.ref_rmanager_trace(cap, ops)
+    assert [m[0] for m in mine] == [r[0] for r in ref_all]
+    assert any(m[0] == 0 for m in mine[:len(ops)])  # the trace hit pool exhaustion
+    st.close()
+
+
 # ------------------------------------------------------------- K1 partials
 
 @pytest.mark.parametrize("dtype", [0, 1, 2])

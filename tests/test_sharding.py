@@ -74,3 +74,65 @@ def test_bench_rank_shares_cover_every_config(cfg, n):
         # placement-limited: the home keeps >= 50% of the long request
         home_tokens = sum(rr.tokens for rr in per[0] if rr.request == 0)
         assert home_tokens >= w.lens[0] // 2
+
+
+# ---- pinned to the compiled reference (oracle/_ref) ----
+needs_ref = pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+def test_blocks_for_tokens_bit_exact_with_reference():
+    """kvsched::perf::blocks_for_tokens (perfmodel.cpp:178-182), the compiled
+    reference, against the product's sizing rule and the C oracle."""
+    import paper_2401_02669_b200 as pb
+    rng = np.random.default_rng(5)
+    toks = [0, 1, 15, 16, 17, 31, 32, 33, 4095, 4096, 4097, 131072, 524288, 1048576, (1 << 40) + 3]
+    toks += [int(x) for x in rng.integers(0, 1 << 31, 200)]
+    for bs in (1, 3, 16, 32, 64, 128):
+        for t in toks:
+            want = oracle.ref_blocks_for_tokens(t, bs)
+            assert pb.blocks_for_tokens(t, bs) == want
+            assert oracle.blocks_for_tokens(t, bs) == want
+
+
+@needs_ref
+def test_cfg5_fixture_is_the_reference_control_planes_output():
+    """tests/golden/cfg5_placement.json regenerates bit-for-bit from the
+    reference (dispatch + heartbeats + GManager::plan + execute_move_sync)."""
+    import importlib.util
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "make_cfg5_placement.py")
+    spec = importlib.util.spec_from_file_location("make_cfg5_placement", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    with open(os.path.join(os.path.dirname(__file__), "golden", "cfg5_placement.json")) as f:
+        committed = json.load(f)
+    assert json.loads(json.dumps(mod.generate())) == committed
+
+
+def test_cfg5_reference_placement_shapes():
+    """Config 5 from the fixture: the planner lends only while freed blocks admit
+    queued requests (scheduler.cpp:62-80), keeps >= 50 % at home
+    (scheduler.cpp:425-431), and at 2 instances finds no creditor below 0.8
+    utilisation (scheduler.hpp:52-58)."""
+    from paper_2401_02669_b200.sharding import gmanager_placement
+    w = workloads.config("5")
+    lens = w.lens
+    nb0 = 32768
+    for n in (2, 4, 8):
+        for q, lent_want in ((0, 0), (64, 2048 if n > 2 else 0), (512, 16384 if n > 2 else 0)):
+            homes, lent = gmanager_placement(lens, n, q)
+            assert homes[0] == 0
+            assert sum(b for (r, _), b in lent.items() if r == 0) == lent_want
+            assert all(r == 0 for (r, _) in lent)  # only the long request lends
+            per = placement_from_moves(lens, homes, lent, n, 16)
+            assert coverage_ok(per, lens)
+            home_tok = sum(rr.tokens for rr in per[0] if rr.request == 0)
+            assert home_tok == (nb0 - lent_want) * 16
+            # the shorts sit on the other instances (most-free dispatch)
+            assert all(h != 0 for h in homes[1:])
+    with pytest.raises(ValueError):
+        gmanager_placement(lens, 3, 64)
+    with pytest.raises(ValueError):
+        gmanager_placement(lens[:-1], 4, 64)
