@@ -347,3 +347,64 @@ def test_exchange_timeout_and_abort_do_not_trap():
         p.join(timeout=120)
     for rank, ok, exc in res:
         assert ok, (rank, exc)
+
+
+def _cfg5_worker(rank, world, port, q):
+    """Config 5 at full size, sharded by the reference control plane's
+    placement (tests/golden/cfg5_placement.json, debtor queue 64), K5 exchange."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import paper_2401_02669_b200 as pb
+    from paper_2401_02669_b200 import workloads
+    try:
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        w = workloads.config("5", 64)
+        shares = workloads.rank_shares(w, world)[rank]
+        pages = sum(-(-rr.tokens // 16) for rr in shares) + 8
+        st = pb.Store(128, 32, 32, pb.BF16, 16, pages, max_seqs=w.batch + 2,
+                      max_pages_per_seq=max(-(-rr.tokens // 16) for rr in shares) + 2, device=rank)
+        st.set_stream(torch.cuda.current_stream().cuda_stream)
+        ranges = []
+        for rr in shares:
+            sq = st.seq_create(rr.tokens)
+            st.fill_synthetic(sq, w.seed, rr.request, rr.tok_begin, w.amp_k, w.amp_v)
+            ranges.append(pb.Range(sq, rr.request, 0, rr.tokens))
+        qd = torch.empty(w.batch, 32, 128, dtype=torch.bfloat16, device=f"cuda:{rank}")
+        st.q_fill_synthetic(qd, w.batch, w.seed)
+        out = torch.zeros_like(qd)
+        uid = [pb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.comm_init(uid[0], rank, world)
+        for _ in range(3):
+            st.decode_sharded(ranges, w.batch, qd, out)
+        torch.cuda.synchronize()
+        par = bench.parity_check(w, out.float().cpu().numpy(), w.lens) if rank == 0 else {"pass": True}
+        q.put((rank, par["pass"], None if par["pass"] else repr(par)))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, False, repr(e)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_full_size_config5_reference_placement():
+    import torch.multiprocessing as mp
+    world = max(n for n in (2, 4, 8) if n <= _ngpus())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_cfg5_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, exc in res:
+        assert ok, (rank, exc)

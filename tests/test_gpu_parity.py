@@ -564,6 +564,32 @@ def test_full_size_config3_tcgen05_vs_cuda_cores(torch_cuda):
     assert rel_errs(got[:1], ref) < 2e-2
 
 
+def test_full_size_config5_single_gpu(torch_cuda):
+    """BASELINE config 5 at full size on one B200 (1 x 524,288 + 256 x 2,048
+    tokens, MHA 32x128, bf16, 16 GiB of KV): sampled (row, q head) outputs --
+    the long request, the first and last short ones and seeded picks -- match
+    the fp64 oracle (bench.parity_check, the check bench.py runs on every line)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2401_02669_b200 as pb
+    from paper_2401_02669_b200 import workloads
+    torch = torch_cuda
+    w = workloads.config("5")
+    pages = sum(-(-L // 16) for L in w.lens) + 8
+    st = pb.Store(128, 32, 32, pb.BF16, 16, pages, max_seqs=w.batch + 2, max_pages_per_seq=-(-max(w.lens) // 16) + 2)
+    st.set_stream(torch.cuda.current_stream().cuda_stream)
+    seqs = [st.seq_create(L) for L in w.lens]
+    for b, sq in enumerate(seqs):
+        st.fill_synthetic(sq, w.seed, b, 0, w.amp_k, w.amp_v)
+    q = torch.empty(w.batch, 32, 128, dtype=torch.bfloat16, device="cuda")
+    st.q_fill_synthetic(q, w.batch, w.seed, 0, 1.0)
+    out = decode(torch, st, [pb.Range(sq, b, 0, L) for b, (sq, L) in enumerate(zip(seqs, w.lens))], w.batch, q)
+    par = bench.parity_check(w, out.float().cpu().numpy(), w.lens)
+    assert 0 in par["rows_checked"] and par["pass"], par
+    st.close()
+
+
 def test_default_stream_ordering(torch_cuda):
     """A store given torch's default-stream handle (0) orders its launches
     after the caller's default-stream work: an output buffer zeroed behind a
