@@ -559,10 +559,14 @@ def run_b200_arm(args, rank, ws, local):
     st.stats(reset=True)
     brk[:] = [0.0, 0.0, 0.0]
     barrier()
+    per_step = []
     t0 = time.perf_counter()
     for t in range(3, 3 + ke):
+        c = time.perf_counter()
         loop_step(t)
+        per_step.append(time.perf_counter() - c)
     t_loop = max_over_ranks(time.perf_counter() - t0) / ke
+    per_step.sort()
     plan_bytes = st.stats().last_plan_bytes
     lens_now = [L + grow_total for L in w.lens]
     out_d = oh.clone()
@@ -619,7 +623,9 @@ def run_b200_arm(args, rank, ws, local):
                         "(plan rebuilt and uploaded) with H2D q and D2H output",
                 "h2d_split": {"q": qbytes, "kv_rows_rank0": app_bytes, "plan_rank0": plan_bytes},
                 "host_ms_rank0": {"kv_append_call": 1e3 * brk[0] / ke, "range_build": 1e3 * brk[1] / ke,
-                                  "decode_call": 1e3 * brk[2] / ke}},
+                                  "decode_call": 1e3 * brk[2] / ke},
+                "step_ms_rank0": {"median": 1e3 * per_step[len(per_step) // 2],
+                                  "p90": 1e3 * per_step[int(0.9 * (len(per_step) - 1))], "max": 1e3 * per_step[-1]}},
         "e2e_static": {"value": w.batch / t_static, "unit": "tokens/s", "ms_per_step": t_static * 1e3,
                        "h2d_bytes_per_step": qbytes, "d2h_bytes_per_step": qbytes,
                        "what": "fixed batch repeated (plan cached), H2D q + D2H output"},

@@ -68,7 +68,7 @@ int64_t dattn_launch_count(int reset);
  * (distattention.hpp:33-42) and the RManager block ledger's capacity
  * (controlplane.hpp:126-134). */
 typedef struct dattn_store_config {
-    int head_dim;          /* >= 1; rows are zero-padded to padded_dim */
+    int head_dim;          /* 1..512; rows are zero-padded to padded_dim */
     int num_q_heads;       /* >= 1 */
     int num_kv_heads;      /* >= 1, divides num_q_heads */
     double scale;          /* 0 -> 1/sqrt(head_dim) (distattention.cpp:35-37) */
@@ -81,7 +81,7 @@ typedef struct dattn_store_config {
 } dattn_store_config;
 
 typedef struct dattn_store_info {
-    int padded_dim;        /* row length in elements (16, 32, 64, 128 or 256) */
+    int padded_dim;        /* row length in elements (16, 32, 64, 128, 256 or 512) */
     int elem_bytes;
     int record_elems;      /* partial record length = padded_dim + 4 */
     int record_bytes;
@@ -117,7 +117,9 @@ typedef struct dattn_stats {
     int64_t last_items, last_chunks, last_plan_bytes;
     int32_t last_chunk_tokens, ma_grid;
     int32_t last_kernel;        /* 1: K1 CUDA-core MA (fp32 / fp64 / other head dims),
-                                   2: K2 tcgen05 MA (bf16, d = 128, any group 1..16) */
+                                   2: K2 tcgen05 MA (bf16, d = 128, any group 1..16),
+                                   3: K1g generic MA (groups above 16, or 8 for fp64;
+                                      head_dim 257..512) */
     int32_t last_exchange;      /* 0: fused merge inside the MA kernel (1 GPU), 1: NCCL allgather + K3,
                                    2: K5 NVLink exchange, 3: MA-kernel group push + K6 rank merge */
     int64_t comm_timed;

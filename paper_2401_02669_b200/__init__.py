@@ -254,10 +254,10 @@ def effective_scale(head_dim: int, scale: float = 0.0) -> float:
 
 
 def padded_dim(head_dim: int) -> int:
-    for dp in (16, 32, 64, 128, 256):
+    for dp in (16, 32, 64, 128, 256, 512):
         if head_dim <= dp:
             return dp
-    raise ContractError(ERR_CONTRACT, "head_dim must be <= 256")
+    raise ContractError(ERR_CONTRACT, "head_dim must be <= 512")
 
 
 class RangeArray:

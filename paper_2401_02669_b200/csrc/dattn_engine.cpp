@@ -42,12 +42,16 @@ static void nccl_check(ncclResult_t r, const char* what) {
 
 void count_launch(int n) { g_launches += n; }
 
+// Scratch buffers grow geometrically: a decode loop whose plan or chunk count
+// creeps up by a few words per step reallocates (a synchronising cudaFree /
+// cudaFreeHost) O(log) times, not at every step that crosses a boundary.
 void DevBuf::ensure(size_t bytes) {
     if (bytes <= cap) return;
     if (p) cudaFree(p);
     p = nullptr;
+    const size_t grown = cap + cap / 2;
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
+    size_t want = std::max<size_t>({bytes, grown, 256});
     cuda_check(cudaMalloc(&p, want), "cudaMalloc");
     cap = want;
 }
@@ -58,8 +62,9 @@ void HostBuf::ensure(size_t bytes) {
     if (bytes <= cap) return;
     if (p) cudaFreeHost(p);
     p = nullptr;
+    const size_t grown = cap + cap / 2;
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
+    size_t want = std::max<size_t>({bytes, grown, 256});
     cuda_check(cudaMallocHost(&p, want), "cudaMallocHost");
     cap = want;
 }
@@ -68,7 +73,7 @@ HostBuf::~HostBuf() {
 }
 
 int padded_dim_for(int head_dim) {
-    for (int dp : {16, 32, 64, 128, 256})
+    for (int dp : {16, 32, 64, 128, 256, 512})
         if (head_dim <= dp) return dp;
     return -1;
 }
@@ -232,8 +237,8 @@ dattn_store::~dattn_store() {
 void dattn_store::activate() const { cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice"); }
 
 static void validate_config(const dattn_store_config& c) {
-    if (c.head_dim < 1 || c.head_dim > 256)
-        throw Error(DATTN_ERR_CONTRACT, "head_dim must be in [1, 256]");
+    if (c.head_dim < 1 || c.head_dim > 512)
+        throw Error(DATTN_ERR_CONTRACT, "head_dim must be in [1, 512]");
     if (c.num_q_heads < 1 || c.num_kv_heads < 1)
         throw Error(DATTN_ERR_CONTRACT, "head counts must be >= 1");
     if (c.num_q_heads % c.num_kv_heads != 0)
@@ -247,9 +252,6 @@ static void validate_config(const dattn_store_config& c) {
     if (c.max_seqs < 1 || c.max_pages_per_seq < 1)
         throw Error(DATTN_ERR_CONTRACT, "block-table shape must be >= 1");
     if (c.num_kv_heads > 255) throw Error(DATTN_ERR_CONTRACT, "num_kv_heads must be <= 255");
-    const int g = c.num_q_heads / c.num_kv_heads;
-    if (g > (c.dtype == kF64 ? 8 : 16))
-        throw Error(DATTN_ERR_CONTRACT, "query group size too large for the MA kernel");
 }
 
 void dattn_store::init(const dattn_store_config& c) {
@@ -288,6 +290,14 @@ void dattn_store::init(const dattn_store_config& c) {
     for (int64_t i = c.num_pages - 1; i >= 0; --i) free_pages.push_back(static_cast<int32_t>(i));
     for (int i = c.max_seqs - 1; i >= 0; --i) free_seqs.push_back(i);
 
+    // K1 covers groups up to 16 (8 for fp64) and rows up to 256 wide; other
+    // shapes run on the generic K1g (MQA, head_dim 257..512)
+    ma_generic = !ma_supported(c.dtype, dp, group);
+    if (ma_generic) {
+        int occ = 0;
+        cuda_check(ma_generic_occupancy(c.dtype, dp, &occ), "occupancy(K1g)");
+        ma_ctas_per_sm = std::max(1, occ);
+    }
     // MA launch geometry: the deepest ring that still fits the target CTAs/SM.
     const char* env_ctas = std::getenv("DATTN_MA_CTAS");
     const char* env_stages = std::getenv("DATTN_MA_STAGES");
@@ -300,12 +310,14 @@ void dattn_store::init(const dattn_store_config& c) {
         if ((need + 1024) * want_ctas <= sm_total && need <= 232448) stages = s;
     }
     if (env_stages) stages = std::max(2, std::atoi(env_stages));
-    ma_stages = stages;
-    ma_smem = ma_smem_bytes(c.dtype, dp, group, stages);
-    cuda_check(ma_configure(c.dtype, dp, group, ma_smem), "cudaFuncSetAttribute(MA)");
-    int occ = 0;
-    cuda_check(ma_occupancy(c.dtype, dp, group, ma_smem, &occ), "occupancy(MA)");
-    ma_ctas_per_sm = std::max(1, occ);
+    if (!ma_generic) {
+        ma_stages = stages;
+        ma_smem = ma_smem_bytes(c.dtype, dp, group, stages);
+        cuda_check(ma_configure(c.dtype, dp, group, ma_smem), "cudaFuncSetAttribute(MA)");
+        int occ = 0;
+        cuda_check(ma_occupancy(c.dtype, dp, group, ma_smem, &occ), "occupancy(MA)");
+        ma_ctas_per_sm = std::max(1, occ);
+    }
 
     // K2: tcgen05 tiles for grouped queries (bf16, d = 128, pages dividing the 128-token tile)
     // MHA (group 1) too: Q is padded to the MMA's N = 16 like any group, and
@@ -497,42 +509,54 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
         pl.any_empty_group |= pl.words[pl.off_expect + i] == 0;
     // claim order: longest item first (LPT), so a ragged batch ends on short
     // items instead of one CTA finishing a long one alone; uniform items keep
-    // the natural order (no table)
+    // the natural order (no table). Every chunk but a range's last is exactly
+    // C tokens, so the order is: all full chunks in natural item order, then
+    // the partial last chunks by length, longest first (ties in item order) --
+    // a stable sort of the items by length, built from the ranges directly.
     pl.off_table = 0;
     if (!one_chunk_per_range && items > 1) {
-        std::vector<std::pair<int32_t, int32_t>> len_item;  // (-tokens, item)
-        len_item.reserve(static_cast<size_t>(items));
+        struct Tail {
+            int32_t len, range;
+        };
+        std::vector<Tail> tails;  // ranges whose last chunk is shorter than C
         int32_t lmin = INT32_MAX, lmax = 0;
         for (int i = 0; i < nr; ++i) {
             const dattn_range& r = b.ranges[i];
             const int64_t len = r.tok_end - r.tok_begin;
-            const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
-            const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
-            const int32_t base = pl.words[pl.off_item + i];
-            for (int64_t j = 0; j < nch; ++j) {
-                const int32_t t = static_cast<int32_t>(std::min<int64_t>(C, len - j * C));
-                lmin = std::min(lmin, t);
-                lmax = std::max(lmax, t);
-                for (int h = 0; h < nh; ++h)
-                    len_item.emplace_back(-t, base + static_cast<int32_t>(j * nh + h));
-            }
+            if (len <= 0) continue;
+            const int32_t last = static_cast<int32_t>(len - (len - 1) / C * C);
+            lmax = std::max<int32_t>(lmax, len > C ? static_cast<int32_t>(C) : last);
+            lmin = std::min(lmin, last);
+            if (last < C) tails.push_back({last, i});
         }
         if (lmax > lmin) {
-            std::stable_sort(len_item.begin(), len_item.end(),
-                             [](const auto& a, const auto& b2) { return a.first < b2.first; });
+            std::stable_sort(tails.begin(), tails.end(), [](const Tail& a, const Tail& b2) { return a.len > b2.len; });
             if (pl.words.size() & 1) pl.words.push_back(0);  // 8-B aligned pairs
             pl.off_table = pl.words.size();
-            pl.words.resize(pl.off_table + 2 * len_item.size());
-            for (size_t k = 0; k < len_item.size(); ++k) {
-                const int32_t item = len_item[k].second;
-                // range of the item: the last range whose first item <= item
-                int lo = 0, hi = nr;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) / 2;
-                    if (pl.words[pl.off_item + mid] <= item) lo = mid; else hi = mid;
+            pl.words.resize(pl.off_table + 2 * static_cast<size_t>(items));
+            int32_t* tab = &pl.words[pl.off_table];
+            size_t k = 0;
+            for (int i = 0; i < nr; ++i) {  // full chunks, natural order
+                const dattn_range& r = b.ranges[i];
+                const int64_t len = r.tok_end - r.tok_begin;
+                if (len <= 0) continue;
+                const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
+                const int64_t nfull = len / C;
+                for (int64_t l = 0; l < nfull * nh; ++l) {
+                    tab[2 * k] = i;
+                    tab[2 * k + 1] = static_cast<int32_t>(l);
+                    ++k;
                 }
-                pl.words[pl.off_table + 2 * k] = lo;
-                pl.words[pl.off_table + 2 * k + 1] = item - pl.words[pl.off_item + lo];
+            }
+            for (const Tail& t : tails) {  // partial last chunks, longest first
+                const dattn_range& r = b.ranges[t.range];
+                const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
+                const int64_t j = (r.tok_end - r.tok_begin - 1) / C;
+                for (int h = 0; h < nh; ++h) {
+                    tab[2 * k] = t.range;
+                    tab[2 * k + 1] = static_cast<int32_t>(j * nh + h);
+                    ++k;
+                }
             }
         }
     }
@@ -570,6 +594,7 @@ void dattn_store::upload_plan(const Plan& pl) {
 bool dattn_store::fused_ok(const Plan& pl, bool check_finite) const {
     (void)pl;
     (void)check_finite;
+    if (ma_generic && !tc_ok) return false;  // K1g has no merge warp
     const char* env = std::getenv("DATTN_FUSED_K1");
     return env && std::atoi(env) == 1;
 }
@@ -635,6 +660,8 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     if (ev) cuda_check(cudaEventRecord(ev[0], stream), "cudaEventRecord");
     if (use_tc)
         cuda_check(launch_gqa_tc(tm_k, tm_v, tm_q, tm_k4, tm_v4, p, grid, stream), "launch(K2 tcgen05)");
+    else if (ma_generic)
+        cuda_check(launch_ma_generic(cfg.dtype, dp, p, grid, stream), "launch(K1g)");
     else
         cuda_check(launch_ma(cfg.dtype, dp, p, grid, ma_smem, stream), "launch(MA)");
     if (ev) cuda_check(cudaEventRecord(ev[1], stream), "cudaEventRecord");
@@ -647,7 +674,7 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     stats.last_chunks = pl.nchunks;
     stats.last_chunk_tokens = pl.chunk_tokens;
     stats.ma_grid = grid;
-    stats.last_kernel = use_tc ? 2 : 1;
+    stats.last_kernel = use_tc ? 2 : (ma_generic ? 3 : 1);
 }
 
 double dattn_store::effective_scale() const {

@@ -66,6 +66,7 @@ struct dattn_store {
     cudaEvent_t meta_ev = nullptr;
     int num_sms = 0;
     int ma_stages = 0, ma_ctas_per_sm = 1;
+    bool ma_generic = false;  // K1g instead of K1 (groups > 16 / 8 fp64, head_dim > 256)
     size_t ma_smem = 0;
 
     void* kpool = nullptr;

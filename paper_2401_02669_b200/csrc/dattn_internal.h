@@ -202,6 +202,10 @@ cudaError_t ma_configure(int dtype, int dp, int group, size_t smem);
 cudaError_t ma_occupancy(int dtype, int dp, int group, size_t smem, int* blocks_per_sm);
 cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t smem,
                       cudaStream_t st);
+// K1g: generic MA for groups K1 does not instantiate and head widths > 256
+bool ma_supported(int dtype, int dp, int group);
+cudaError_t ma_generic_occupancy(int dtype, int dp, int* blocks_per_sm);
+cudaError_t launch_ma_generic(int dtype, int dp, const MAParams& p, int grid, cudaStream_t st);
 cudaError_t launch_merge(int dtype, int dp, const MergeParams& p, cudaStream_t st);
 cudaError_t launch_merge_exchange(int dtype, int dp, const XParams& p, int grid, cudaStream_t st);
 // Resident CTAs per SM of K5 (kind 0) / K6 (kind 1): their polls need the

@@ -544,6 +544,118 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     if (nonfinite && p.nonfinite_flag) atomicOr(p.nonfinite_flag, 1);
 }
 
+// ------------------------------------------------------------------ K1g
+// Generic micro-attention for the shapes K1's shared-memory pipeline does not
+// instantiate: query groups above 16 (8 for fp64 stores; MQA such as 32 q / 1
+// kv head) and padded head widths above 256. Same work items, claim protocol
+// (the counter advances by nitems + grid per launch) and records as K1: a CTA
+// claims an item (range, chunk, kv head); each of its warps owns q heads
+// h = warp, warp + 4, ... of the group, streams the chunk's K/V rows through
+// L1 (warps of one CTA share them), reduces q.k across the warp and keeps an
+// online softmax in registers (lane l owns dims l, l + 32, ...). Correct for
+// every shape the reference accepts up to head_dim 512; not a roofline kernel.
+constexpr int kGenericWarps = 4;
+
+template <typename T, int DP>
+__global__ void __launch_bounds__(32 * kGenericWarps) ma_generic_kernel(const MAParams p) {
+    using E = Elem<T>;
+    using Acc = typename E::Acc;
+    constexpr int EPL = (DP + 31) / 32;
+    constexpr int REC = DP + 4;
+    pdl_launch_dependents();
+    __shared__ int s_item;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const T* kpool = static_cast<const T*>(p.k_pool);
+    const T* vpool = static_cast<const T*>(p.v_pool);
+    const T* qg = static_cast<const T*>(p.q);
+    const int P = p.page_tokens;
+    const Acc scale_log2 = static_cast<Acc>(p.scale_log2);
+    const Acc kLn2 = static_cast<Acc>(0.6931471805599453094);
+    const Acc kNegInf = -static_cast<Acc>(INFINITY);
+    Acc* recs = static_cast<Acc*>(p.records);
+    bool nonfinite = false;
+    for (;;) {
+        __syncthreads();  // everyone has read the previous s_item
+        if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= p.nitems) break;
+        int r, local;
+        if (p.item_table) {
+            const int2 ent = __ldg(reinterpret_cast<const int2*>(p.item_table) + item);
+            r = ent.x;
+            local = ent.y;
+        } else {
+            r = find_range(p.item_prefix, p.nranges, item);
+            local = item - __ldg(p.item_prefix + r);
+        }
+        const RangeDev rg = p.ranges[r];
+        const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
+        const int j = local / nh;
+        const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
+        const int tlo = rg.lo + j * p.chunk_tokens;
+        const int thi = min(rg.hi, tlo + p.chunk_tokens);
+        const int gchunk = __ldg(p.chunk_prefix + r) + j;
+        const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
+        for (int h = warp; h < p.group; h += kGenericWarps) {
+            const T* qs = qg + (static_cast<int64_t>(rg.out_row) * p.num_q_heads +
+                                static_cast<int64_t>(kvh) * p.group + h) * DP;
+            Acc q[EPL], acc[EPL];
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) {
+                const int jd = lane + 32 * i;
+                q[i] = jd < DP ? E::to_acc(qs[jd]) * scale_log2 : Acc(0);
+                acc[i] = 0;
+            }
+            Acc m = kNegInf, e = 0;
+            for (int t = tlo; t < thi; ++t) {
+                const int64_t page = __ldg(bt + t / P);
+                const int64_t row = ((page * p.num_kv_heads + kvh) * P + t % P) * DP;
+                Acc sc = 0;
+#pragma unroll
+                for (int i = 0; i < EPL; ++i) {
+                    const int jd = lane + 32 * i;
+                    if (jd < DP) {
+                        const Acc x = E::to_acc(kpool[row + jd]);
+                        if constexpr (std::is_same<T, double>::value) nonfinite |= !isfinite(x);
+                        sc += q[i] * x;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
+                const Acc mx = sc > m ? sc : m;
+                const Acc corr = (mx == m) ? Acc(1) : acc_exp2(m - mx);
+                const Acc pw = acc_exp2(sc - mx);
+                e = e * corr + pw;
+                m = mx;
+#pragma unroll
+                for (int i = 0; i < EPL; ++i) {
+                    const int jd = lane + 32 * i;
+                    if (jd < DP) {
+                        const Acc x = E::to_acc(vpool[row + jd]);
+                        if constexpr (std::is_same<T, double>::value) nonfinite |= !isfinite(x);
+                        acc[i] = acc[i] * corr + pw * x;
+                    }
+                }
+            }
+            Acc* rec = recs + ((static_cast<int64_t>(gchunk) * p.num_q_heads + static_cast<int64_t>(kvh) * p.group + h) *
+                               REC);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) {
+                const int jd = lane + 32 * i;
+                if (jd < DP) rec[4 + jd] = acc[i];
+            }
+            if (lane == 0) {
+                rec[0] = m * kLn2;
+                rec[1] = e;
+                rec[2] = static_cast<Acc>(thi - tlo);
+                rec[3] = 0;
+            }
+        }
+    }
+    if (nonfinite && p.nonfinite_flag) atomicOr(p.nonfinite_flag, 1);
+}
+
 // ------------------------------------------------------------------ K3
 // One CTA (8 warps) per (row, q head) group. Pass 1: block max over live
 // records. Pass 2: warp w folds records w, w+8, ... with vector loads (each
@@ -1149,6 +1261,7 @@ __global__ void identity_records_kernel(Acc* recs, int64_t n) {
         case 64: { constexpr int DPC = 64; __VA_ARGS__; } break;   \
         case 128: { constexpr int DPC = 128; __VA_ARGS__; } break; \
         case 256: { constexpr int DPC = 256; __VA_ARGS__; } break; \
+        case 512: { constexpr int DPC = 512; __VA_ARGS__; } break; \
         default: return cudaErrorInvalidValue;        \
     }
 #define DATTN_DT_SWITCH(dt, ...)                                 \
@@ -1161,12 +1274,31 @@ __global__ void identity_records_kernel(Acc* recs, int64_t n) {
 
 template <typename T, int DP>
 static const void* ma_fn(int group) {
-    if (group <= kConsumerWarps) return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 1>);
-    if constexpr (sizeof(T) < 8) {
-        if (group <= 2 * kConsumerWarps)
-            return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 2>);
+    if constexpr (DP <= 256) {  // K1's instantiations; wider rows take K1g
+        if (group <= kConsumerWarps) return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 1>);
+        if constexpr (sizeof(T) < 8) {
+            if (group <= 2 * kConsumerWarps)
+                return reinterpret_cast<const void*>(&ma_decode_kernel<T, DP, 2>);
+        }
     }
     return nullptr;
+}
+
+static const void* ma_kernel_ptr(int dtype, int dp, int group);
+bool ma_supported(int dtype, int dp, int group) { return ma_kernel_ptr(dtype, dp, group) != nullptr; }
+
+cudaError_t ma_generic_occupancy(int dtype, int dp, int* blocks_per_sm) {
+    cudaError_t e = cudaSuccess;
+    *blocks_per_sm = 0;
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                                     blocks_per_sm, ma_generic_kernel<TC, DPC>,
+                                                     32 * kGenericWarps, 0))));
+    return e;
+}
+
+cudaError_t launch_ma_generic(int dtype, int dp, const MAParams& p, int grid, cudaStream_t st) {
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (ma_generic_kernel<TC, DPC><<<grid, 32 * kGenericWarps, 0, st>>>(p))));
+    return cudaGetLastError();
 }
 
 static const void* ma_kernel_ptr(int dtype, int dp, int group) {

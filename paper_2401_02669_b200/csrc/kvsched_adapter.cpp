@@ -54,9 +54,9 @@ void raise(dattn_status st) {
 #define DATTN_CALL(expr) raise(expr)
 
 int padded(int d) {
-    for (int dp : {16, 32, 64, 128, 256})
+    for (int dp : {16, 32, 64, 128, 256, 512})
         if (d <= dp) return dp;
-    throw ContractError("head_dim > 256 is not supported by the B200 kernels");
+    throw ContractError("head_dim > 512 is not supported by the B200 kernels");
 }
 
 // One fp64 store per (padded dim, query group) and calling thread, grown on
@@ -319,7 +319,6 @@ std::vector<double> multi_head_attention(
             "kv head count mismatch");
     const int d = cfg.head_dim, dp = padded(d);
     const int hkv = cfg.num_kv_heads, g = cfg.num_q_heads / hkv;
-    if (g > 8) throw ContractError("query group > 8 is not supported by the fp64 kernels");
     int64_t pages = 0;
     int nseg = 0;
     for (const auto& segs : kv_segments_per_head) {

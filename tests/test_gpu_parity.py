@@ -590,6 +590,82 @@ def test_full_size_config5_single_gpu(torch_cuda):
     st.close()
 
 
+# ------------------------------------------------ shapes beyond K1 / K2 (K1g)
+
+@pytest.mark.parametrize("hq,hkv,d,dtype", [
+    (32, 1, 128, 0),   # MQA, bf16: group 32
+    (64, 2, 128, 1),   # group 32, fp32
+    (16, 1, 64, 2),    # fp64 group 16
+    (4, 2, 300, 0),    # head_dim 300 (padded 512), bf16
+    (4, 4, 512, 1),    # head_dim 512, fp32
+    (8, 2, 257, 2),    # head_dim 257, fp64, group 4
+])
+def test_generic_ma_shapes_vs_oracle(torch_cuda, hq, hkv, d, dtype):
+    """Query groups above what K1 / K2 instantiate (MQA) and head_dim 257..512
+    run on K1g; outputs match the oracle (the reference accepts any group and
+    head_dim, distattention.cpp:39-46, 176-209)."""
+    import oracle
+    import paper_2401_02669_b200 as pb
+    torch = torch_cuda
+    lens = [1, 700, 2100]
+    st, seqs, q = make(torch, lens, hq, hkv, d, dtype, seed=91)
+    rg = [pb.Range(seqs[0], 0, 0, 1), pb.Range(seqs[1], 1, 0, 700), pb.Range(seqs[2], 2, 0, 1000),
+          pb.Range(seqs[2], 2, 1000, 2100)]
+    out = out_np(torch, decode(torch, st, rg, 3, q), d)
+    assert st.stats().last_kernel == 3
+    ref = oracle.decode_ranges(91, [0] * 3, lens, [0, 1, 2], hq, hkv, d, dtype=dtype)
+    assert rel_errs(out, ref) < TOL[dtype]
+    st.close()
+
+
+@pytest.fixture(scope="module")
+def dropin(tmp_path_factory):
+    import ctypes
+    import shutil
+    lib = os.path.join(ROOT, "paper_2401_02669_b200", "_lib")
+    if not shutil.which("g++"):
+        pytest.skip("needs g++")
+    so = str(tmp_path_factory.mktemp("dropin") / "libdropin_probe.so")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-shared", "-fPIC", f"-I{ROOT}/include",
+                    os.path.join(ROOT, "tests", "dropin_probe.cpp"), "-o", so, f"-L{lib}", "-ldattn",
+                    f"-Wl,-rpath,{lib}"], check=True, capture_output=True)
+    return ctypes.CDLL(so)
+
+
+@pytest.mark.skipif(not __import__("oracle").ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("hq,hkv,d", [(32, 1, 16), (24, 2, 40), (12, 1, 64), (4, 2, 300), (2, 1, 512)])
+def test_dropin_multi_head_attention_large_groups_and_dims(torch_cuda, dropin, hq, hkv, d):
+    """kvsched::attn::multi_head_attention of the drop-in (fp64 on the GPU) vs
+    the compiled reference on identical inputs: groups above 8 and head_dim
+    above 256, which round 1 rejected, within the reference's own 1e-10."""
+    import ctypes
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(hq * 1000 + d)
+    seq = 333
+    q = rng.uniform(-1, 1, (hq, d))
+    k = rng.uniform(-1, 1, (hkv, seq, d)) * 3
+    v = rng.uniform(-2, 2, (hkv, seq, d))
+    cuts, ncuts = [], []
+    for h in range(hkv):
+        c = sorted({0, seq, *rng.integers(0, seq, 3).tolist()})
+        cuts += c
+        ncuts.append(len(c) - 1)
+    cf = np.ascontiguousarray(cuts, dtype=np.int64)
+    nc = np.ascontiguousarray(ncuts, dtype=np.int32)
+    got = np.zeros(hq * d)
+    ref = np.zeros(hq * d)
+    P = ctypes.c_void_p
+    f = dropin.dropin_multi_head_attention
+    f.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, P, P, P]
+    assert f(q.ctypes.data, k.ctypes.data, v.ctypes.data, seq, hq, hkv, d, 0.0, cf.ctypes.data, nc.ctypes.data,
+             got.ctypes.data) == 0
+    rc = oracle.ref().ref_multi_head_attention(q.ctypes.data, k.ctypes.data, v.ctypes.data, seq, hq, hkv, d, 0.0,
+                                               cf.ctypes.data, nc.ctypes.data, ref.ctypes.data)
+    assert rc == 0
+    assert rel_errs(got.reshape(hq, d), ref.reshape(hq, d)) < 1e-10
+
+
 def test_default_stream_ordering(torch_cuda):
     """A store given torch's default-stream handle (0) orders its launches
     after the caller's default-stream work: an output buffer zeroed behind a
