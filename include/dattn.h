@@ -303,6 +303,57 @@ dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const vo
 dattn_status dattn_kv_send(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
 dattn_status dattn_kv_recv(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
 
+/* ------------------------------------------------ block placement ledger */
+
+/* The cluster's block ledger and the decode loop's slot rule (SURVEY §8f
+ * row 3): one RManager block ledger per instance (GPU)
+ * (controlplane.cpp:38-79, free_blocks controlplane.hpp:130) plus the
+ * simulator's per-step ensure_slot (simengine.cpp:318-354): a request's next
+ * token takes a block at its home when the home has one, otherwise -- under a
+ * borrowing policy -- on another instance ("overflow borrowing"): one that
+ * already hosts blocks of the request first, then the one with the most free
+ * blocks among instances none of whose own requests borrow, then any
+ * instance with room. Host-only (no GPU). The ledger also records where each
+ * block went, in allocation order, so every instance knows which token
+ * positions of a request it holds: dattn_ledger_segments gives the token
+ * ranges a rank passes to dattn_decode_sharded. Not thread-safe. */
+typedef struct dattn_ledger dattn_ledger;
+
+/* n_instances >= 1 instances with capacity_blocks[i] >= 0 blocks each, blocks
+ * of block_tokens tokens (perfmodel.cpp:178-182 sizing). */
+dattn_status dattn_ledger_create(int n_instances, const int64_t* capacity_blocks, int block_tokens,
+                                 dattn_ledger** out);
+void dattn_ledger_destroy(dattn_ledger* l);
+/* try_admit (simengine.cpp:262-268): alloc_local(blocks_for_tokens(tokens))
+ * at `home`; *admitted = 0 when the home lacks room (nothing changes).
+ * tokens >= 1; req must not be live. */
+dattn_status dattn_ledger_admit(dattn_ledger* l, int64_t req, int home, int64_t tokens, int* admitted);
+/* ensure_slot: a block for the request's next token (position ctx). Returns
+ * the instance that holds position ctx in *instance, or -1 when no instance
+ * can take the block (the reference's stalled request; with allow_borrow = 0
+ * the static_alloc policy: home only). */
+dattn_status dattn_ledger_ensure_slot(dattn_ledger* l, int64_t req, int allow_borrow, int* instance);
+/* The step wrote `tokens` new tokens of req (on_step_done's ctx++,
+ * simengine.cpp:444-452); the request must hold their blocks. */
+dattn_status dattn_ledger_advance(dattn_ledger* l, int64_t req, int64_t tokens);
+/* free_request on every instance (complete, simengine.cpp:300-303). */
+dattn_status dattn_ledger_release(dattn_ledger* l, int64_t req, int64_t* freed_blocks);
+/* RManager accessors: capacity_blocks / used_blocks / free_blocks of one
+ * instance, and the blocks of req it holds (local_blocks on the home,
+ * hosted_blocks(req, home) elsewhere). */
+dattn_status dattn_ledger_instance(const dattn_ledger* l, int instance, int64_t* capacity, int64_t* used,
+                                   int64_t* free_blocks);
+dattn_status dattn_ledger_request(const dattn_ledger* l, int64_t req, int* home, int64_t* ctx,
+                                  int64_t* held_blocks);
+dattn_status dattn_ledger_blocks(const dattn_ledger* l, int64_t req, int instance, int64_t* blocks);
+/* Token ranges [tok_begin, tok_end) of positions [0, ctx) of req in block
+ * order, consecutive blocks on one instance merged: *n ranges (at most max
+ * written; *n is the full count). */
+dattn_status dattn_ledger_segments(const dattn_ledger* l, int64_t req, int max, int* instance,
+                                   int64_t* tok_begin, int64_t* tok_end, int* n);
+/* summary_.overflow_borrows: blocks allocated remotely so far. */
+dattn_status dattn_ledger_borrowed(const dattn_ledger* l, int64_t* blocks);
+
 /* --------------------------------------------------------- verification */
 
 /* kvs_verify_attention (kvsched.h:56-62, capi.cpp:141-155) on the GPU path:

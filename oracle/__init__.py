@@ -265,6 +265,8 @@ def ref():
             "ref_rmanager_trace": [I64, ctypes.c_int, VP, VP, VP, VP, VP, VP, VP, VP],
             "ref_cfg5_place": [ctypes.c_int, I64, I64, ctypes.c_int, ctypes.c_int, VP, VP, VP,
                                ctypes.c_int, VP, VP, VP],
+            "ref_sim_log": [ctypes.c_int, VP, ctypes.c_int, ctypes.c_int, VP, VP, VP, D,
+                            ctypes.POINTER(ctypes.c_void_p)],
         }.items():
             f = getattr(r, n)
             f.restype = ctypes.c_int
@@ -355,3 +357,28 @@ def ref_cfg5_place(tokens: Sequence[int], n_inst: int, capacity_blocks: int, que
                dst_instance=int(moves[6 * i + 3]), num_blocks=int(moves[6 * i + 4]),
                moved_blocks=int(moves[6 * i + 5]), est_gain=float(gains[i])) for i in range(min(int(nm[0]), maxm))]
     return [int(h) for h in home], blocks.reshape(n_req, n_inst).tolist(), mv
+
+
+SIM_INFINITE, SIM_STRAWMAN, SIM_STATIC = 0, 1, 2
+
+
+def ref_sim_log(capacities: Sequence[int], requests, policy: int = SIM_STRAWMAN, horizon_s: float = 1e5):
+    """Run the reference cluster simulator (run_simulation, simengine.cpp) on
+    ``requests`` = [(arrival_s, prompt_tokens, output_tokens)] (ids 0..n-1)
+    over instances with the given block capacities, default model
+    (config.cpp:71-87). Returns the parsed JSONL event log."""
+    import json
+    r = ref()
+    caps = np.ascontiguousarray(capacities, dtype=np.int64)
+    arr = np.ascontiguousarray([q[0] for q in requests], dtype=np.float64)
+    pr = np.ascontiguousarray([q[1] for q in requests], dtype=np.int64)
+    out = np.ascontiguousarray([q[2] for q in requests], dtype=np.int64)
+    p = ctypes.c_void_p()
+    rc = r.ref_sim_log(len(caps), _p(caps), policy, len(requests), _p(arr), _p(pr), _p(out), horizon_s,
+                       ctypes.byref(p))
+    if rc != 0:
+        raise ValueError(r.ref_last_error().decode())
+    text = ctypes.string_at(p.value).decode()
+    r.ref_string_free.argtypes = [ctypes.c_void_p]
+    r.ref_string_free(p)
+    return [json.loads(line) for line in text.splitlines() if line.strip()]

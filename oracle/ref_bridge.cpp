@@ -13,12 +13,15 @@
 // perfmodel.cpp:178-182) and (5) produce config 5's placement with the
 // reference's own dispatch + rManager heartbeats + gManager plan_round +
 // execute_move_sync (simengine.cpp:252-257, controlplane.cpp:412-485,
-// scheduler.cpp:483-493, controlplane.cpp:518-540).
+// scheduler.cpp:483-493, controlplane.cpp:518-540), (6) run the reference
+// cluster simulator (simengine.cpp) to pin the overflow-borrowing slot rule
+// (ensure_slot, simengine.cpp:318-354) of the B200 block ledger.
 #include "kvsched/common.hpp"
 #include "kvsched/config.hpp"
 #include "kvsched/controlplane.hpp"
 #include "kvsched/distattention.hpp"
 #include "kvsched/perfmodel.hpp"
+#include "kvsched/simengine.hpp"
 #include "kvsched/trace.hpp"
 #include "kvsched/verify.hpp"
 
@@ -27,6 +30,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <sstream>
+#include <unistd.h>
 #include <memory>
 #include <string>
 #include <thread>
@@ -260,6 +266,47 @@ int ref_default_config_json(int n_instances, int64_t capacity_blocks, char** out
 }
 
 void ref_string_free(char* p) { std::free(p); }
+
+// The reference simulator (run_simulation, simengine.cpp) on a hand-made
+// trace: n_inst instances with capacity caps[i] blocks each, the default
+// model (config.cpp:71-87), policy 0 infinite / 1 strawman / 2 static, and
+// requests (arrival[i], prompt[i], output[i]) with ids 0..n_req-1. *log_out
+// = the JSONL event log without "msg" lines (admit / prefill_done / borrow /
+// step / complete ...),
+// malloc'ed, freed with ref_string_free.
+int ref_sim_log(int n_inst, const int64_t* caps, int policy, int n_req, const double* arrival,
+                const int64_t* prompt, const int64_t* output, double horizon_s, char** log_out) {
+    return guarded([&] {
+        sim::ClusterConfig cc = sim::default_cluster_config(n_inst, caps[0]);
+        for (int i = 0; i < n_inst; ++i) cc.instances[i].capacity_blocks = caps[i];
+        cc.policy = policy == 0 ? sim::Policy::infinite
+                  : policy == 1 ? sim::Policy::strawman : sim::Policy::static_alloc;
+        std::vector<sim::TraceRequest> trace(n_req);
+        for (int i = 0; i < n_req; ++i) {
+            trace[i].req_id = i;
+            trace[i].arrival_s = arrival[i];
+            trace[i].prompt_tokens = prompt[i];
+            trace[i].output_tokens = output[i];
+        }
+        char path[] = "/tmp/ref_sim_log_XXXXXX";
+        const int fd = mkstemp(path);
+        if (fd < 0) throw std::runtime_error("mkstemp failed");
+        close(fd);
+        sim::RunOptions opt;
+        opt.horizon_s = horizon_s;
+        opt.event_log_path = path;
+        (void)sim::run_simulation(cc, trace, opt);
+        // keep every event but the control-plane message traffic ("msg")
+        std::ifstream f(path, std::ios::binary);
+        std::string t, line;
+        while (std::getline(f, line))
+            if (line.find("\"ev\":\"msg\"") == std::string::npos) t += line + "\n";
+        std::remove(path);
+        *log_out = static_cast<char*>(std::malloc(t.size() + 1));
+        std::memcpy(*log_out, t.c_str(), t.size() + 1);
+    });
+}
+
 
 // Parse a cluster config with the reference parser (parse_cluster_config,
 // config.cpp:111-183, which validates every curve) and evaluate its

@@ -156,6 +156,19 @@ _FUNCS = {
                                             ctypes.c_void_p, ctypes.c_int]),
     "dattn_kv_send": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
     "dattn_kv_recv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
+    "dattn_ledger_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "dattn_ledger_destroy": (None, [ctypes.c_void_p]),
+    "dattn_ledger_admit": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]),
+    "dattn_ledger_ensure_slot": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "dattn_ledger_advance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64]),
+    "dattn_ledger_release": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_ledger_instance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_ledger_request": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_ledger_blocks": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]),
+    "dattn_ledger_segments": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "dattn_ledger_borrowed": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "dattn_verify_attention": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                               ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int)]),
     "dattn_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
@@ -467,6 +480,87 @@ class Store:
 
     def kv_recv(self, seq: int, tok0: int, n: int, peer: int):
         check(lib.dattn_kv_recv(self._h, seq, tok0, n, peer))
+
+
+class Ledger:
+    """The cluster block ledger + the decode loop's slot rule (include/dattn.h
+    "block placement ledger"): one RManager ledger per instance
+    (controlplane.cpp:38-79) and ensure_slot's overflow borrowing
+    (simengine.cpp:318-354). Host-only; usable without a GPU."""
+
+    def __init__(self, capacity_blocks: Sequence[int], block_tokens: int = 16):
+        caps = (ctypes.c_int64 * len(capacity_blocks))(*capacity_blocks)
+        h = ctypes.c_void_p()
+        check(lib.dattn_ledger_create(len(capacity_blocks), caps, block_tokens, ctypes.byref(h)))
+        self._h = h
+        self.n_instances = len(capacity_blocks)
+        self.block_tokens = block_tokens
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.dattn_ledger_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def admit(self, req: int, home: int, tokens: int) -> bool:
+        a = ctypes.c_int()
+        check(lib.dattn_ledger_admit(self._h, req, home, tokens, ctypes.byref(a)))
+        return bool(a.value)
+
+    def ensure_slot(self, req: int, allow_borrow: bool = True) -> int:
+        """Instance holding the request's next token position, -1 if stalled."""
+        i = ctypes.c_int()
+        check(lib.dattn_ledger_ensure_slot(self._h, req, 1 if allow_borrow else 0, ctypes.byref(i)))
+        return i.value
+
+    def advance(self, req: int, tokens: int = 1):
+        check(lib.dattn_ledger_advance(self._h, req, tokens))
+
+    def release(self, req: int) -> int:
+        f = ctypes.c_int64()
+        check(lib.dattn_ledger_release(self._h, req, ctypes.byref(f)))
+        return f.value
+
+    def instance(self, i: int):
+        """(capacity, used, free) blocks of instance i."""
+        c, u, f = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib.dattn_ledger_instance(self._h, i, ctypes.byref(c), ctypes.byref(u), ctypes.byref(f)))
+        return c.value, u.value, f.value
+
+    def free_blocks(self, i: int) -> int:
+        return self.instance(i)[2]
+
+    def request(self, req: int):
+        """(home, ctx tokens, held blocks)."""
+        h, c, b = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib.dattn_ledger_request(self._h, req, ctypes.byref(h), ctypes.byref(c), ctypes.byref(b)))
+        return h.value, c.value, b.value
+
+    def blocks(self, req: int, inst: int) -> int:
+        n = ctypes.c_int64()
+        check(lib.dattn_ledger_blocks(self._h, req, inst, ctypes.byref(n)))
+        return n.value
+
+    def segments(self, req: int):
+        """[(instance, tok_begin, tok_end)] of positions [0, ctx), block order."""
+        n = ctypes.c_int()
+        check(lib.dattn_ledger_segments(self._h, req, 0, None, None, None, ctypes.byref(n)))
+        k = n.value
+        inst = (ctypes.c_int * max(k, 1))()
+        lo = (ctypes.c_int64 * max(k, 1))()
+        hi = (ctypes.c_int64 * max(k, 1))()
+        check(lib.dattn_ledger_segments(self._h, req, k, inst, lo, hi, ctypes.byref(n)))
+        return [(inst[i], lo[i], hi[i]) for i in range(k)]
+
+    def borrowed(self) -> int:
+        n = ctypes.c_int64()
+        check(lib.dattn_ledger_borrowed(self._h, ctypes.byref(n)))
+        return n.value
 
 
 def comm_unique_id() -> bytes:

@@ -966,26 +966,6 @@ void dattn_store::decode_sharded(const dattn_batch& b, const void* q, void* out,
 
 // ------------------------------------------------------------------ C ABI
 
-template <class F>
-static dattn_status guarded(F&& f) {
-    try {
-        f();
-        return DATTN_OK;
-    } catch (const Error& e) {
-        set_error(e.what());
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        set_error("out of host memory");
-        return DATTN_ERR_INTERNAL;
-    } catch (const std::exception& e) {
-        set_error(e.what());
-        return DATTN_ERR_INTERNAL;
-    }
-}
-
-#define REQUIRE_ARG(cond, msg) \
-    do { if (!(cond)) throw Error(DATTN_ERR_INVALID_ARGUMENT, msg); } while (0)
-
 extern "C" {
 
 const char* dattn_last_error(void) { return g_last_error.c_str(); }

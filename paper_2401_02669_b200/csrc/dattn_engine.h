@@ -25,6 +25,27 @@ void count_launch(int n);
 int padded_dim_for(int head_dim);
 int elem_bytes_for(int dtype);
 
+// C ABI wrapper: exceptions -> status + thread-local message (capi.cpp:43-55)
+template <class F>
+inline dattn_status guarded(F&& f) {
+    try {
+        f();
+        return DATTN_OK;
+    } catch (const Error& e) {
+        set_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_error("out of host memory");
+        return DATTN_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return DATTN_ERR_INTERNAL;
+    }
+}
+
+#define REQUIRE_ARG(cond, msg) \
+    do { if (!(cond)) throw ::dattn::Error(DATTN_ERR_INVALID_ARGUMENT, msg); } while (0)
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;

@@ -27,6 +27,43 @@ def _port():
     return p
 
 
+def _run_ranks(target, args, world, timeout):
+    """Start one spawned process per rank, collect one result tuple each.
+    A rank that has not reported after `timeout` s dumps its Python stack to
+    stderr (faulthandler, armed in _arm_watchdog) and is killed; the assertion
+    names the silent ranks and carries the results that did arrive."""
+    import queue
+    import time
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res, deadline = [], time.monotonic() + timeout
+    while len(res) < world:
+        try:
+            res.append(q.get(timeout=max(1.0, deadline - time.monotonic())))
+        except queue.Empty:
+            break
+    for p in procs:
+        p.join(timeout=60 if len(res) == world else 5)
+        if p.is_alive():
+            p.kill()
+            p.join(timeout=10)
+    got = sorted(r[0] for r in res)
+    assert len(res) == world, f"ranks {sorted(set(range(world)) - set(got))} never reported; received {sorted(res)}"
+    return sorted(res)
+
+
+def _arm_watchdog(seconds):
+    """Dump every thread's stack and exit if this worker is still running
+    after `seconds` (the parent reports the rank as silent)."""
+    import faulthandler
+    faulthandler.dump_traceback_later(seconds, exit=True)
+
+
 MODES = {"k5_nvlink": {"DATTN_FUSED_MERGE": "1"}, "nccl": {"DATTN_FUSED_MERGE": "0"},
          "k1_push_k6": {"DATTN_FUSED_MERGE": "1", "DATTN_FUSED_K1": "1"}}
 
@@ -50,7 +87,9 @@ def _worker(rank, world, port, case, placement, fused, q):
     import paper_2401_02669_b200 as pb
     from paper_2401_02669_b200.sharding import placement_from_moves, plan_rank_ranges
 
+    _arm_watchdog(560)
     try:
+        os.environ.setdefault("DATTN_EXCHANGE_TIMEOUT_S", "20")
         os.environ.update(MODES[fused])
         torch.cuda.set_device(rank)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -154,17 +193,8 @@ def _worker(rank, world, port, case, placement, fused, q):
 @pytest.mark.parametrize("placement", [False, True])
 @pytest.mark.parametrize("fused", sorted(MODES))
 def test_sharded_decode_matches_oracle(case, placement, fused):
-    import torch.multiprocessing as mp
     world = min(_ngpus(), 8)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, placement, fused, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=600) for _ in procs)
-    for p in procs:
-        p.join(timeout=120)
+    res = _run_ranks(_worker, (case, placement, fused,), world, 600)
     for rank, err, agree, same, exc in res:
         assert exc is None, (rank, exc)
         assert agree and same, (rank, agree)
@@ -190,6 +220,7 @@ def _migrate_worker(rank, world, port, q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         seed, L, hq, hkv, d = 808, 1000, 8, 4, 128
+        _arm_watchdog(560)
         split = 512  # tokens [512, 1000) move from rank 0 to rank 1
         st = pb.Store(d, hq, hkv, pb.BF16, 16, 128, max_seqs=4, max_pages_per_seq=80, device=rank)
         st.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -234,17 +265,8 @@ def _migrate_worker(rank, world, port, q):
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_kv_block_migration_between_gpus():
-    import torch.multiprocessing as mp
     world = min(_ngpus(), 8)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=600) for _ in procs)
-    for p in procs:
-        p.join(timeout=120)
+    res = _run_ranks(_migrate_worker, (), world, 600)
     for rank, err, ok, exc in res:
         assert exc is None, (rank, exc)
         assert ok
@@ -265,6 +287,7 @@ def _abort_worker(rank, world, port, q):
     import torch.distributed as dist
 
     import paper_2401_02669_b200 as pb
+    _arm_watchdog(560)
     try:
         os.environ["DATTN_EXCHANGE_TIMEOUT_S"] = "2"
         os.environ["DATTN_FUSED_MERGE"] = "1"
@@ -334,17 +357,8 @@ def _abort_worker(rank, world, port, q):
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_exchange_timeout_and_abort_do_not_trap():
-    import torch.multiprocessing as mp
     world = min(_ngpus(), 8)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_abort_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=600) for _ in procs)
-    for p in procs:
-        p.join(timeout=120)
+    res = _run_ranks(_abort_worker, (), world, 600)
     for rank, ok, exc in res:
         assert ok, (rank, exc)
 
@@ -361,6 +375,7 @@ def _cfg5_worker(rank, world, port, q):
     import bench
     import paper_2401_02669_b200 as pb
     from paper_2401_02669_b200 import workloads
+    _arm_watchdog(860)
     try:
         torch.cuda.set_device(rank)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -395,16 +410,7 @@ def _cfg5_worker(rank, world, port, q):
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_full_size_config5_reference_placement():
-    import torch.multiprocessing as mp
     world = max(n for n in (2, 4, 8) if n <= _ngpus())
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_cfg5_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=900) for _ in procs)
-    for p in procs:
-        p.join(timeout=120)
+    res = _run_ranks(_cfg5_worker, (), world, 900)
     for rank, ok, exc in res:
         assert ok, (rank, exc)
