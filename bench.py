@@ -85,6 +85,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="decode-loop steps (0: min(--steps, 64))")
     ap.add_argument("--chunk-tokens", type=int, default=0)
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check (profiling runs)")
+    ap.add_argument("--migration-pages", default="1,16,128,512",
+                    help="N>1: pages pulled per decode step in the migration-overlap sweep ('' skips it)")
     return ap.parse_args()
 
 
@@ -175,6 +177,57 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _, _ in rows),
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
                 "power_w_max": pmax}
+
+
+class NvlinkCounters:
+    """NVLink data bytes moved by this GPU (NVML field values
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed over links):
+    read before and after a region, so a multi-GPU line carries the bytes that
+    actually crossed NVLink next to the algorithmic exchange bytes."""
+
+    def __init__(self, index: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.links = [l for l in range(18)
+                          if self._ok(lambda: pynvml.nvmlDeviceGetNvLinkState(self.h, l))]
+        except Exception:
+            self.h = None
+
+    @staticmethod
+    def _ok(f):
+        try:
+            return bool(f())
+        except Exception:
+            return False
+
+    def read(self):
+        """(tx_bytes, rx_bytes) since boot, or None."""
+        if self.h is None or not self.links:
+            return None
+        try:
+            nv = self.nv
+            req = [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l) for l in self.links] + \
+                  [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l) for l in self.links]
+            vals = nv.nvmlDeviceGetFieldValues(self.h, req)
+            out = []
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                out.append(int(v.value.ullVal))
+            n = len(self.links)
+            return 1024 * sum(out[:n]), 1024 * sum(out[n:])
+        except Exception:
+            return None
+
+    @staticmethod
+    def delta(a, b, steps):
+        if a is None or b is None:
+            return None
+        return {"tx_bytes_per_step": (b[0] - a[0]) / steps, "rx_bytes_per_step": (b[1] - a[1]) / steps}
 
 
 # ----------------------------------------------------------------- CPU side
@@ -401,8 +454,10 @@ def run_b200_arm(args, rank, ws, local):
                 tail_rank[rr.request] = r_
     mine = [rr.request in tail_rank and tail_rank[rr.request] == rank for rr in shares]
     cap_tokens = [rr.tokens + (grow_total if m else 0) for rr, m in zip(shares, mine)]
-    pages = sum(-(-t // page) for t in cap_tokens) + 16
-    max_pps = max(-(-t // page) for t in cap_tokens) + 2
+    mig_rates = [int(x) for x in args.migration_pages.split(",") if x.strip()] if ws > 1 else []
+    mig_cap = max(mig_rates, default=0)  # destination pages of the migration sweep (a ring)
+    pages = sum(-(-t // page) for t in cap_tokens) + 16 + mig_cap
+    max_pps = max([-(-t // page) for t in cap_tokens] + [mig_cap]) + 2
     st = pb.Store(w.d, w.hq, w.hkv, w.dtype, page, pages, max_seqs=w.batch + 4,
                   max_pages_per_seq=max(max_pps, 1), device=local)
     stream = torch.cuda.Stream(device=local)
@@ -573,6 +628,125 @@ def run_b200_arm(args, rank, ws, local):
     qbytes = qh.numel() * qh.element_size()
     app_bytes = 2 * n_app * w.hkv * st.padded_dim * st.elem_bytes
 
+    # ---- region E (N > 1): paced block migration overlapped with decode ----
+    # Every rank pulls m whole pages (K+V, all kv heads) of its left
+    # neighbour's pool per decode step (dattn_kv_pull: copy engines over
+    # NVLink, migration stream) while it decodes the same batch; the step
+    # joins its pulls, so a step costs max(decode, copies). m = 1 page is the
+    # reference's pacing (MigrationConfig step_tokens 16, config.hpp:44-51).
+    # The destination is a ring of m pages; sources are real pages the decode
+    # also reads. Same device timing as region A (max over ranks).
+    migration = None
+    if mig_rates:
+        src_seq = max(range(len(shares)), key=lambda i: shares[i].tokens)
+        my_pages = st.block_table(seqs[src_seq])
+        all_pages = [None] * ws
+        dist.all_gather_object(all_pages, my_pages)
+        left = (rank + ws - 1) % ws
+        src_pages = all_pages[left][:-1]  # full pages only (a sequence's last page may be partial)
+        dst = st.seq_create(mig_cap * page)
+        km = max(10, min(args.steps, 50))
+        page_bytes = 2 * w.hkv * page * st.padded_dim * st.elem_bytes
+        sweep = []
+        for m in [0] + mig_rates:
+            if m > len(src_pages):
+                continue
+            pulls = [src_pages[(j * m) % (len(src_pages) - m + 1):][:m] for j in range(km + 3)]
+
+            def mstep(j):
+                if m:
+                    st.kv_pull(dst, 0, left, pulls[j])
+                step()
+                if m:
+                    st.migration_join()
+
+            for j in range(3):
+                mstep(j)
+            torch.cuda.synchronize()
+            barrier()
+            m0 = torch.cuda.Event(enable_timing=True)
+            m1 = torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            for j in range(3, 3 + km):
+                mstep(j)
+            m1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            t_m = max_over_ranks(m0.elapsed_time(m1)) / km
+            sweep.append({"pages_per_step": m, "tokens_per_step": m * page,
+                          "bytes_per_step_per_rank": m * page_bytes, "ms_per_step": t_m,
+                          "nvlink_gbs_per_rank": m * page_bytes / (t_m * 1e-3) / 1e9})
+        # the last pull's first and last pages hold the generator's values of
+        # the left neighbour's tokens, bit for bit (oracle, outside the timing)
+        st.migration_join(wait_host=True)
+        pulled_ok = None
+        last = pulls[km + 2]
+        if last and not args.no_parity:
+            import oracle
+            lsh = all_shares[left]
+            lrr = lsh[max(range(len(lsh)), key=lambda i: lsh[i].tokens)]
+            pulled_ok = True
+            for slot in (0, len(last) - 1):
+                p_idx = src_pages.index(last[slot])
+                for h in (0, w.hkv - 1):
+                    k_, v_ = st.kv_read(dst, h, slot * page, page)
+                    rk, rv = oracle.synth_kv(w.seed, lrr.request, h, lrr.tok_begin + p_idx * page, page, w.d,
+                                             w.amp_k, w.amp_v, w.dtype)
+                    pulled_ok &= bool(np.array_equal(k_[:, :w.d], rk[:, :w.d]) and np.array_equal(v_[:, :w.d], rv[:, :w.d]))
+        oks = [None] * ws
+        dist.all_gather_object(oks, pulled_ok)
+        base = sweep[0]["ms_per_step"]
+        for e_ in sweep:
+            e_["slowdown_vs_no_migration"] = e_["ms_per_step"] / base - 1.0
+        migration = {"what": "each rank pulls m pages/step of its left neighbour's KV pool (dattn_kv_pull, copy "
+                             "engines over NVLink) while decoding the batch; step = decode + join of its pulls",
+                     "page_bytes": page_bytes, "sweep": sweep, "pulled_pages_bit_exact": oks,
+                     "reference_model": "MigrationConfig: 16 tokens/step hidden (overlap_cap_tokens), then "
+                                        "+0.086/16 step per extra token (config.hpp:44-51)"}
+
+    # ---- region F (N > 1, after every timed region): NVLink bytes per step ----
+    # NVML's NVLink throughput counters, read around K untimed steps of the
+    # benchmarked batch (and of the largest migration rate). Kept out of the
+    # timed regions: with the counters queried, a 2-GPU config-2 step measured
+    # 1.40 ms instead of 1.18 ms on the same box.
+    nvlink = None
+    if ws > 1 and os.environ.get("BENCH_NVLINK", "1") != "0":
+        nvl = NvlinkCounters(local)
+        kf = max(10, min(args.steps, 50))
+
+        def counted(fn):
+            torch.cuda.synchronize()
+            barrier()
+            a = nvl.read()
+            for j in range(kf):
+                fn(j)
+            torch.cuda.synchronize()
+            b = nvl.read()
+            barrier()
+            return NvlinkCounters.delta(a, b, kf)
+
+        live = sum(1 for rr in shares if rr.tokens) * w.hq
+        mine_alg = (ws - 1) * (live * st.record_bytes + (w.batch * w.hq - live) * 16)
+        nv_dec = counted(lambda j: step())
+        nv_mig = None
+        if mig_rates:
+            mmax = max(m for m in mig_rates if m <= len(src_pages))
+
+            def pull_step(j):
+                st.kv_pull(dst, 0, left, src_pages[(j * mmax) % (len(src_pages) - mmax + 1):][:mmax])
+                step()
+                st.migration_join()
+            nv_mig = counted(pull_step)
+            nv_mig = {"pages_per_step": mmax, "alg_bytes_per_step": mmax * page_bytes, **(nv_mig or {})}
+        per = [None] * ws
+        dist.all_gather_object(per, [nv_dec, mine_alg, nv_mig])
+        nvlink = {"decode_counters_per_rank": [p_[0] for p_ in per],
+                  "exchange_alg_bytes_per_rank": [p_[1] for p_ in per],
+                  "migration_counters_per_rank": [p_[2] for p_ in per],
+                  "what": "NVML NVLink data TX/RX bytes per step, untimed steps after the timed regions; "
+                          "algorithmic: K5 pushes one record per (row, q head) to every peer (identity "
+                          "records only their 16-byte header); migration: pulled pages x page bytes"}
+
     # ---- parity of what was timed (outside every timed region) ----
     parity = parity_loop = None
     if rank == 0 and not args.no_parity:
@@ -638,6 +812,10 @@ def run_b200_arm(args, rank, ws, local):
     }
     if comm:
         line["comm"] = comm
+    if nvlink:
+        line["nvlink"] = nvlink
+    if migration:
+        line["migration"] = migration
     if ws == 1 and not args.no_cpu_baseline:
         cv, info = cpu_reference_sample(w, args.cpu_seconds)
         c1, info1 = cpu_reference_sample(w, min(args.cpu_seconds, 4.0), threads=1)

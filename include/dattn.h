@@ -303,6 +303,23 @@ dattn_status dattn_decode_sharded(dattn_store* s, const dattn_batch* b, const vo
 dattn_status dattn_kv_send(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
 dattn_status dattn_kv_recv(dattn_store* s, int32_t seq, int64_t tok0, int64_t n, int peer);
 
+/* Block migration overlapped with decode (the same protocol's data path, as
+ * the paper runs it: KV moves while the source keeps decoding, PAPER.md:1451;
+ * paced by advance_transfers, controlplane.cpp:205-225). The receiver pulls
+ * n_pages whole pages -- K and V, all kv heads -- of a peer's pool, source
+ * page ids src_pages (the sender's dattn_seq_block_table entries, passed by
+ * the host), into its own sequence dst_seq at page-aligned position dst_tok0
+ * (dst_seq must already hold those pages). The copies go over NVLink on the
+ * copy engines from a low-priority migration stream (both pools are
+ * IPC-mapped at dattn_comm_init), so they take no SMs from the decode
+ * kernels, and the call returns at once. dattn_kv_migration_join orders the
+ * store stream's later work after every pull issued so far (and, with
+ * wait_host, blocks until they are done); the sender must keep the source
+ * pages until then. A partly filled last page is copied whole. */
+dattn_status dattn_kv_pull(dattn_store* s, int32_t dst_seq, int64_t dst_tok0, int src_rank,
+                          const int32_t* src_pages, int64_t n_pages);
+dattn_status dattn_kv_migration_join(dattn_store* s, int wait_host);
+
 /* ------------------------------------------------ block placement ledger */
 
 /* The cluster's block ledger and the decode loop's slot rule (SURVEY §8f

@@ -156,6 +156,9 @@ _FUNCS = {
                                             ctypes.c_void_p, ctypes.c_int]),
     "dattn_kv_send": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
     "dattn_kv_recv": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
+    "dattn_kv_pull": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_int64]),
+    "dattn_kv_migration_join": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "dattn_ledger_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_void_p)]),
     "dattn_ledger_destroy": (None, [ctypes.c_void_p]),
@@ -480,6 +483,16 @@ class Store:
 
     def kv_recv(self, seq: int, tok0: int, n: int, peer: int):
         check(lib.dattn_kv_recv(self._h, seq, tok0, n, peer))
+
+    def kv_pull(self, dst_seq: int, dst_tok0: int, src_rank: int, src_pages: Sequence[int]):
+        """Copy whole pages of src_rank's pool into dst_seq at dst_tok0 over
+        NVLink (copy engines, migration stream; returns at once)."""
+        arr = (ctypes.c_int32 * max(len(src_pages), 1))(*src_pages)
+        check(lib.dattn_kv_pull(self._h, dst_seq, dst_tok0, src_rank, ctypes.cast(arr, ctypes.c_void_p),
+                                len(src_pages)))
+
+    def migration_join(self, wait_host: bool = False):
+        check(lib.dattn_kv_migration_join(self._h, 1 if wait_host else 0))
 
 
 class Ledger:

@@ -94,6 +94,57 @@ void dattn_store::release_exchange() {
     fused_merge = false;
 }
 
+void dattn_store::release_peer_pools() {
+    if (mig_stream) cudaStreamSynchronize(mig_stream);
+    for (int r = 0; r < 8; ++r) {
+        if (r != rank) {
+            if (peer_kpool[r]) cudaIpcCloseMemHandle(peer_kpool[r]);
+            if (peer_vpool[r]) cudaIpcCloseMemHandle(peer_vpool[r]);
+        }
+        peer_kpool[r] = peer_vpool[r] = nullptr;
+    }
+    mig_pending = 0;
+}
+
+// Map every rank's K and V pools into this process (CUDA IPC, handles
+// all-gathered over the communicator) so dattn_kv_pull can copy a peer's
+// pages straight into this store's pages over NVLink.
+void dattn_store::setup_peer_pools() {
+    release_peer_pools();
+    const char* env = std::getenv("DATTN_PEER_POOLS");
+    if ((env && std::atoi(env) == 0) || nranks > kMaxRanks) return;
+    if (!mig_stream) {
+        int lo = 0, hi = 0;
+        cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+        cuda_check(cudaStreamCreateWithPriority(&mig_stream, cudaStreamNonBlocking, lo), "cudaStreamCreate(mig)");
+        cuda_check(cudaEventCreateWithFlags(&mig_ev, cudaEventDisableTiming), "cudaEventCreate(mig)");
+    }
+    constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+    cudaIpcMemHandle_t h[2];
+    cuda_check(cudaIpcGetMemHandle(&h[0], kpool), "cudaIpcGetMemHandle(k)");
+    cuda_check(cudaIpcGetMemHandle(&h[1], vpool), "cudaIpcGetMemHandle(v)");
+    std::vector<unsigned char> all(2 * kH * nranks);
+    DevBuf dh;
+    dh.ensure(all.size());
+    unsigned char* mine = static_cast<unsigned char*>(dh.p) + rank * 2 * kH;
+    cuda_check(cudaMemcpyAsync(mine, h, 2 * kH, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync");
+    nccl_check(ncclAllGather(mine, dh.p, 2 * kH, ncclUint8, comm, comm_begin()), "ncclAllGather(pool handles)");
+    comm_end();
+    cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) {
+            peer_kpool[r] = kpool;
+            peer_vpool[r] = vpool;
+            continue;
+        }
+        cudaIpcMemHandle_t px[2];
+        std::memcpy(px, all.data() + r * 2 * kH, 2 * kH);
+        cuda_check(cudaIpcOpenMemHandle(&peer_kpool[r], px[0], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(k)");
+        cuda_check(cudaIpcOpenMemHandle(&peer_vpool[r], px[1], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(v)");
+    }
+}
+
 // Order NCCL work after `stream`'s queued work, on the comm stream; comm_end()
 // orders later `stream` work after it.
 cudaStream_t dattn_store::comm_begin() {
@@ -212,6 +263,9 @@ dattn_store::~dattn_store() {
         }
     }
     release_exchange();
+    release_peer_pools();
+    if (mig_ev) cudaEventDestroy(mig_ev);
+    if (mig_stream) cudaStreamDestroy(mig_stream);
     if (x_status_host) cudaFreeHost(x_status_host);
     if (x_ctl_dev) cudaFree(x_ctl_dev);
     if (abort_stream) cudaStreamDestroy(abort_stream);
@@ -1390,6 +1444,7 @@ dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE
         // describe it (release_exchange skips the old own rank)
         cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
         s->release_exchange();
+        s->release_peer_pools();
         if (s->comm) ncclCommDestroy(s->comm);
         s->comm = nullptr;
         s->rank = 0;
@@ -1397,7 +1452,10 @@ dattn_status dattn_comm_init(dattn_store* s, const unsigned char id[DATTN_UNIQUE
         nccl_check(ncclCommInitRank(&s->comm, nranks, u, rank), "ncclCommInitRank");
         s->rank = rank;
         s->nranks = nranks;
-        if (nranks > 1) s->setup_exchange();
+        if (nranks > 1) {
+            s->setup_exchange();
+            s->setup_peer_pools();
+        }
     });
 }
 
@@ -1486,6 +1544,62 @@ dattn_status dattn_kv_recv(dattn_store* s, int32_t seq, int64_t tok0, int64_t n,
     return guarded([&] {
         REQUIRE_ARG(s, "null store");
         kv_transfer(s, seq, tok0, n, peer, false);
+    });
+}
+
+dattn_status dattn_kv_pull(dattn_store* s, int32_t dst_seq, int64_t dst_tok0, int src_rank,
+                          const int32_t* src_pages, int64_t n_pages) {
+    return guarded([&] {
+        REQUIRE_ARG(s && (n_pages == 0 || src_pages), "null argument");
+        if (!s->comm) throw Error(DATTN_ERR_CONTRACT, "dattn_comm_init was not called");
+        if (src_rank < 0 || src_rank >= s->nranks || src_rank == s->rank || !s->peer_kpool[src_rank])
+            throw Error(DATTN_ERR_CONTRACT, "bad source rank (or its pool is not mapped)");
+        s->check_seq(dst_seq);
+        const int64_t P = s->cfg.page_tokens;
+        if (n_pages < 0 || dst_tok0 < 0 || dst_tok0 % P != 0)
+            throw Error(DATTN_ERR_CONTRACT, "pulls move whole pages: dst_tok0 must be page aligned");
+        const int64_t p0 = dst_tok0 / P;
+        if (p0 + n_pages > s->seq_pages[dst_seq])
+            throw Error(DATTN_ERR_CONTRACT, "destination pages outside the sequence");
+        for (int64_t i = 0; i < n_pages; ++i)
+            if (src_pages[i] < 0 || src_pages[i] >= s->cfg.num_pages)
+                throw Error(DATTN_ERR_CONTRACT, "source page id out of range");
+        if (n_pages == 0) return;
+        s->activate();
+        // the destination pages' earlier writes (allocation, appends) come first
+        cuda_check(cudaEventRecord(s->mig_ev, s->stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s->mig_stream, s->mig_ev, 0), "cudaStreamWaitEvent");
+        const size_t pb = static_cast<size_t>(s->page_elems) * s->esz;
+        const int32_t* bt = s->h_bt.data() + static_cast<size_t>(dst_seq) * s->cfg.max_pages_per_seq;
+        auto* dk = static_cast<unsigned char*>(s->kpool);
+        auto* dv = static_cast<unsigned char*>(s->vpool);
+        auto* sk = static_cast<const unsigned char*>(s->peer_kpool[src_rank]);
+        auto* sv = static_cast<const unsigned char*>(s->peer_vpool[src_rank]);
+        // one copy per run of pages consecutive on both sides (copy engines
+        // over NVLink; no SMs taken from the decode kernels)
+        for (int64_t i = 0; i < n_pages;) {
+            int64_t j = i + 1;
+            while (j < n_pages && src_pages[j] == src_pages[j - 1] + 1 && bt[p0 + j] == bt[p0 + j - 1] + 1) ++j;
+            const size_t bytes = static_cast<size_t>(j - i) * pb;
+            cuda_check(cudaMemcpyAsync(dk + static_cast<size_t>(bt[p0 + i]) * pb, sk + static_cast<size_t>(src_pages[i]) * pb,
+                                       bytes, cudaMemcpyDeviceToDevice, s->mig_stream), "cudaMemcpyAsync(pull k)");
+            cuda_check(cudaMemcpyAsync(dv + static_cast<size_t>(bt[p0 + i]) * pb, sv + static_cast<size_t>(src_pages[i]) * pb,
+                                       bytes, cudaMemcpyDeviceToDevice, s->mig_stream), "cudaMemcpyAsync(pull v)");
+            i = j;
+        }
+        s->mig_pending += n_pages;
+    });
+}
+
+dattn_status dattn_kv_migration_join(dattn_store* s, int wait_host) {
+    return guarded([&] {
+        REQUIRE_ARG(s, "null store");
+        if (!s->mig_stream) return;
+        s->activate();
+        cuda_check(cudaEventRecord(s->mig_ev, s->mig_stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s->stream, s->mig_ev, 0), "cudaStreamWaitEvent");
+        if (wait_host) cuda_check(cudaEventSynchronize(s->mig_ev), "cudaEventSynchronize(mig)");
+        s->mig_pending = 0;
     });
 }
 

@@ -149,6 +149,16 @@ struct dattn_store {
     void check_exchange_status() const;
     void setup_exchange();
     void release_exchange();
+    // KV migration by page copies (dattn_kv_pull): every rank's K/V pools
+    // IPC-mapped here; copies run on the copy engines from mig_stream, a
+    // low-priority stream beside the decode stream
+    void* peer_kpool[8]{};
+    void* peer_vpool[8]{};
+    cudaStream_t mig_stream = nullptr;
+    cudaEvent_t mig_ev = nullptr;
+    int64_t mig_pending = 0;  // pulls issued since the last dattn_kv_migration_join
+    void setup_peer_pools();
+    void release_peer_pools();
 
     // K2 (tcgen05) path for grouped-query bf16 stores
     bool tc_ok = false;

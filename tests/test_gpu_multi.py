@@ -414,3 +414,173 @@ def test_full_size_config5_reference_placement():
     res = _run_ranks(_cfg5_worker, (), world, 900)
     for rank, ok, exc in res:
         assert ok, (rank, exc)
+
+
+def _overflow_worker(rank, world, port, q):
+    """A decode loop whose contexts outgrow their home GPU: the block ledger's
+    ensure_slot (simengine.cpp:318-354) lends blocks on other GPUs, the slot's
+    rank appends the token there, and the sharded decode over home + hosted
+    blocks must match the oracle at the grown lengths. Every rank's free pages
+    must equal its instance's free blocks in the (replicated) ledger."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2401_02669_b200 as pb
+    from paper_2401_02669_b200.decode_loop import ClusterDecodeLoop
+    _arm_watchdog(560)
+    try:
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        seed, hq, hkv, d = 515, 16, 4, 128
+        prompts = [700, 300, 200, 120, 40]
+        # instance 0 has room for the long prompt plus two blocks: its growth
+        # overflows onto the others after ~36 steps (dispatch puts every other
+        # request on the roomier instances, which keep enough free blocks for
+        # their own growth and the loan: no request stalls)
+        caps = [46] + [80] * (world - 1)
+        st = pb.Store(d, hq, hkv, pb.BF16, 16, caps[rank], max_seqs=16, max_pages_per_seq=caps[rank], device=rank)
+        st.set_stream(torch.cuda.current_stream().cuda_stream)
+        uid = [pb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.comm_init(uid[0], rank, world)
+        loop = ClusterDecodeLoop(st, rank, world, caps, seed)
+        assert loop.admit(0, 0, prompts[0], home=0)  # the long request lives on the small instance
+        for i, L in enumerate(prompts[1:], 1):
+            assert loop.admit(i, i, L)  # dispatch: most free blocks
+        B = len(prompts)
+        qd = torch.empty(B, hq, st.padded_dim, dtype=torch.bfloat16, device=f"cuda:{rank}")
+        st.q_fill_synthetic(qd, B, seed)
+        out = torch.zeros_like(qd)
+        checks, ledger_ok, worst = [], True, 0.0
+        for t in range(1, 97):
+            loop.step(B, qd, out)
+            torch.cuda.synchronize()
+            ledger_ok &= st.info().free_pages == loop.led.free_blocks(rank)
+            if t in (1, 40, 96):
+                lens = [loop.led.request(r)[1] for r in range(B)]
+                got = out[..., :d].double().cpu().numpy()
+                g = torch.from_numpy(got)
+                allg = [torch.zeros_like(g) for _ in range(world)]
+                dist.all_gather(allg, g)
+                agree = all(torch.equal(allg[0], x) for x in allg)
+                err = 0.0
+                if rank == 0:
+                    ref = oracle.decode_ranges(seed, [0] * B, lens, list(range(B)), hq, hkv, d, dtype=pb.BF16)
+                    err = max(oracle.rel_err(got[b, h], ref[b, h]) for b in range(B) for h in range(hq))
+                    worst = max(worst, err)
+                checks.append((t, agree, lens))
+        borrowed = loop.led.borrowed()
+        segs0 = loop.led.segments(0)
+        ok = ledger_ok and all(c[1] for c in checks) and borrowed > 0 and len({s[0] for s in segs0}) > 1 \
+            and loop.stalled == 0
+        q.put((rank, worst if rank == 0 else None, ok,
+               None if ok else repr(dict(ledger_ok=ledger_ok, checks=checks, borrowed=borrowed, segs0=segs0,
+                                         stalled=loop.stalled))))
+        dist.destroy_process_group()
+    except Exception as e:
+        import traceback
+        q.put((rank, None, False, traceback.format_exc()))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_decode_loop_overflow_borrowing():
+    world = min(_ngpus(), 8)
+    res = _run_ranks(_overflow_worker, (), world, 600)
+    for rank, err, ok, exc in res:
+        assert ok, (rank, exc)
+        if rank == 0:
+            assert err < 2e-2, err
+
+
+def _pull_worker(rank, world, port, q):
+    """Paced block migration overlapped with decode (dattn_kv_pull): rank 1
+    pulls the tail pages of rank 0's request one page per decode step over
+    NVLink while both keep decoding over the old placement; after the join the
+    pulled pages equal the generator bit-exactly and the decode over the new
+    placement (rank 0 keeps the prefix, rank 1 the tail) matches the oracle and
+    the old placement's output."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2401_02669_b200 as pb
+    _arm_watchdog(560)
+    try:
+        torch.cuda.set_device(rank)
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        seed, L, hq, hkv, d, split = 909, 1000, 8, 4, 128, 512
+        st = pb.Store(d, hq, hkv, pb.BF16, 16, 160, max_seqs=4, max_pages_per_seq=80, device=rank)
+        st.set_stream(torch.cuda.current_stream().cuda_stream)
+        uid = [pb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.comm_init(uid[0], rank, world)
+        none = st.seq_create(0)
+        src = dst = None
+        if rank == 0:
+            # a block table with a gap: another sequence's pages in between
+            src = st.seq_create(600)
+            tmp = st.seq_create(48)
+            st.seq_resize(src, L)
+            st.seq_release(tmp)
+            st.fill_synthetic(src, seed, 0, 0, 1.0, 2.0)
+            pages = st.block_table(src)
+        else:
+            pages = None
+        pages = [pages]
+        dist.broadcast_object_list(pages, src=0)
+        tail_pages = pages[0][split // 16:]
+        if rank == 1:
+            dst = st.seq_create(L - split)
+        qd = torch.empty(1, hq, 128, dtype=torch.bfloat16, device=f"cuda:{rank}")
+        st.q_fill_synthetic(qd, 1, seed)
+        out = torch.zeros_like(qd)
+        old = [pb.Range(src, 0, 0, L)] if rank == 0 else [pb.Range(none, 0, 0, 0)]
+        for i, pg in enumerate(tail_pages):  # one block per decode step (advance_transfers)
+            if rank == 1:
+                st.kv_pull(dst, 16 * i, 0, [pg])
+            st.decode_sharded(old, 1, qd, out)
+        before = out.clone()
+        if rank == 1:
+            st.migration_join()
+        dist.barrier()
+        new = ([pb.Range(src, 0, 0, split)] if rank == 0 else
+               [pb.Range(dst, 0, 0, L - split)] if rank == 1 else [pb.Range(none, 0, 0, 0)])
+        st.decode_sharded(new, 1, qd, out)
+        torch.cuda.synchronize()
+        ok = True
+        if rank == 1:
+            for h in range(hkv):
+                k, v = st.kv_read(dst, h, 0, L - split)
+                rk, rv = oracle.synth_kv(seed, 0, h, split, L - split, d, 1.0, 2.0, pb.BF16)
+                ok &= bool(np.array_equal(k, rk) and np.array_equal(v, rv))
+        err = None
+        if rank == 0:
+            ref = oracle.decode_ranges(seed, [0], [L], [0], hq, hkv, d, dtype=pb.BF16)
+            got = out[..., :d].double().cpu().numpy()
+            err = max(oracle.rel_err(got[0, h], ref[0, h]) for h in range(hq))
+            ok &= float((out.float() - before.float()).abs().max()) < 1e-2
+        q.put((rank, err, ok, None))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, None, False, traceback.format_exc()))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_kv_pull_migration_overlapped_with_decode():
+    world = min(_ngpus(), 8)
+    res = _run_ranks(_pull_worker, (), world, 600)
+    for rank, err, ok, exc in res:
+        assert exc is None and ok, (rank, exc)
+        if rank == 0:
+            assert err < 2e-2, err

@@ -199,3 +199,39 @@ def test_ensure_slot_replays_reference_simulator_random(seed):
             for _ in range(rng.randint(2, 12))]
     log = oracle.ref_sim_log(caps, reqs, oracle.SIM_STRAWMAN, horizon_s=2000)
     replay(caps, reqs, oracle.SIM_STRAWMAN, log)
+
+
+def test_segments_partition_the_context():
+    """After any mix of growth, borrowing and releases, every live request's
+    segments tile [0, ctx) in order, each switch of instance falls on a block
+    boundary (so a hosted sequence's pages are whole blocks), and each
+    instance's used blocks equal the blocks its segments cover."""
+    rng = random.Random(9)
+    caps = [30, 18, 25, 12]
+    led = pb.Ledger(caps, 16)
+    live, nxt = [], 0
+    for _ in range(3000):
+        a = rng.random()
+        if a < 0.05 or not live:
+            home = max(range(4), key=lambda i: (led.free_blocks(i), -i))
+            if led.admit(nxt, home, rng.randint(1, 150)):
+                live.append(nxt)
+            nxt += 1
+        elif a < 0.97:
+            r = rng.choice(live)
+            if led.ensure_slot(r) >= 0:
+                led.advance(r)
+        else:
+            led.release(live.pop(rng.randrange(len(live))))
+        if rng.random() < 0.02:
+            used = [0] * 4
+            for r in live:
+                segs = led.segments(r)
+                _, ctx, held = led.request(r)
+                assert segs[0][1] == 0 and segs[-1][2] == ctx
+                for (i0, _, e0), (i1, b1, _) in zip(segs, segs[1:]):
+                    assert e0 == b1 and i0 != i1 and b1 % 16 == 0
+                for i in range(4):
+                    used[i] += led.blocks(r, i)
+                assert sum(led.blocks(r, i) for i in range(4)) == held
+            assert used == [led.instance(i)[1] for i in range(4)]
