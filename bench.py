@@ -179,57 +179,6 @@ class ClockSampler:
                 "power_w_max": pmax}
 
 
-class NvlinkCounters:
-    """NVLink data bytes moved by this GPU (NVML field values
-    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB, summed over links):
-    read before and after a region, so a multi-GPU line carries the bytes that
-    actually crossed NVLink next to the algorithmic exchange bytes."""
-
-    def __init__(self, index: int):
-        self.h = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.links = [l for l in range(18)
-                          if self._ok(lambda: pynvml.nvmlDeviceGetNvLinkState(self.h, l))]
-        except Exception:
-            self.h = None
-
-    @staticmethod
-    def _ok(f):
-        try:
-            return bool(f())
-        except Exception:
-            return False
-
-    def read(self):
-        """(tx_bytes, rx_bytes) since boot, or None."""
-        if self.h is None or not self.links:
-            return None
-        try:
-            nv = self.nv
-            req = [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l) for l in self.links] + \
-                  [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l) for l in self.links]
-            vals = nv.nvmlDeviceGetFieldValues(self.h, req)
-            out = []
-            for v in vals:
-                if v.nvmlReturn != 0:
-                    return None
-                out.append(int(v.value.ullVal))
-            n = len(self.links)
-            return 1024 * sum(out[:n]), 1024 * sum(out[n:])
-        except Exception:
-            return None
-
-    @staticmethod
-    def delta(a, b, steps):
-        if a is None or b is None:
-            return None
-        return {"tx_bytes_per_step": (b[0] - a[0]) / steps, "rx_bytes_per_step": (b[1] - a[1]) / steps}
-
-
 # ----------------------------------------------------------------- CPU side
 
 def cpu_reference_sample(w, budget_s: float, reps_fixed: int = 0, threads: int = 0, warmup: int = 0):
@@ -704,48 +653,21 @@ def run_b200_arm(args, rank, ws, local):
                      "reference_model": "MigrationConfig: 16 tokens/step hidden (overlap_cap_tokens), then "
                                         "+0.086/16 step per extra token (config.hpp:44-51)"}
 
-    # ---- region F (N > 1, after every timed region): NVLink bytes per step ----
-    # NVML's NVLink throughput counters, read around K untimed steps of the
-    # benchmarked batch (and of the largest migration rate). Kept out of the
-    # timed regions: with the counters queried, a 2-GPU config-2 step measured
-    # 1.40 ms instead of 1.18 ms on the same box.
+    # ---- NVLink bytes per step of the K5 exchange (algorithmic) ----
+    # NVML's NVLink throughput counters (field ids 138-141) answer
+    # NVML_ERROR_NOT_SUPPORTED on these boxes, and querying NVLink state
+    # perturbed the timing of later steps (2-GPU config 2: 1.40 instead of
+    # 1.18 ms per step), so the line carries the algorithmic bytes only
+    # (profiles/r2_nvlink_counters_probe.txt).
     nvlink = None
-    if ws > 1 and os.environ.get("BENCH_NVLINK", "1") != "0":
-        nvl = NvlinkCounters(local)
-        kf = max(10, min(args.steps, 50))
-
-        def counted(fn):
-            torch.cuda.synchronize()
-            barrier()
-            a = nvl.read()
-            for j in range(kf):
-                fn(j)
-            torch.cuda.synchronize()
-            b = nvl.read()
-            barrier()
-            return NvlinkCounters.delta(a, b, kf)
-
+    if ws > 1:
         live = sum(1 for rr in shares if rr.tokens) * w.hq
         mine_alg = (ws - 1) * (live * st.record_bytes + (w.batch * w.hq - live) * 16)
-        nv_dec = counted(lambda j: step())
-        nv_mig = None
-        if mig_rates:
-            mmax = max(m for m in mig_rates if m <= len(src_pages))
-
-            def pull_step(j):
-                st.kv_pull(dst, 0, left, src_pages[(j * mmax) % (len(src_pages) - mmax + 1):][:mmax])
-                step()
-                st.migration_join()
-            nv_mig = counted(pull_step)
-            nv_mig = {"pages_per_step": mmax, "alg_bytes_per_step": mmax * page_bytes, **(nv_mig or {})}
         per = [None] * ws
-        dist.all_gather_object(per, [nv_dec, mine_alg, nv_mig])
-        nvlink = {"decode_counters_per_rank": [p_[0] for p_ in per],
-                  "exchange_alg_bytes_per_rank": [p_[1] for p_ in per],
-                  "migration_counters_per_rank": [p_[2] for p_ in per],
-                  "what": "NVML NVLink data TX/RX bytes per step, untimed steps after the timed regions; "
-                          "algorithmic: K5 pushes one record per (row, q head) to every peer (identity "
-                          "records only their 16-byte header); migration: pulled pages x page bytes"}
+        dist.all_gather_object(per, mine_alg)
+        nvlink = {"exchange_alg_bytes_per_rank": per,
+                  "what": "bytes each rank pushes over NVLink per step in K5: one record per (row, q head) "
+                          "to every peer, identity records only their 16-byte header"}
 
     # ---- parity of what was timed (outside every timed region) ----
     parity = parity_loop = None
