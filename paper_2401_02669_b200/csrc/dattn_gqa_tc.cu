@@ -258,6 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // launched with programmatic serialization behind the previous step's
+    // merge grid: the set-up above (barriers, operand zeroing, TMEM, tensor
+    // maps) overlapped its tail; records, q and the work counter are touched
+    // only after it has completed
+    pdl_wait();
     const uint32_t tmem = S.tmem_base;
     const uint32_t tmem_s = tmem;
     const uint32_t tmem_o0 = tmem + kN;  // O^T of even tiles; odd tiles at + kN
@@ -694,7 +699,7 @@ cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, 
     MAParams pp = p;
     void* args[] = {const_cast<void*>(tm_k), const_cast<void*>(tm_v), const_cast<void*>(tm_q),
                     const_cast<void*>(tm_k4), const_cast<void*>(tm_v4), &pp};
-    return cudaLaunchKernel(gqa_fn(p.group), dim3(grid), dim3(tc::kThreads), args, gqa_tc_smem_bytes(), st);
+    return launch_pdl_raw(gqa_fn(p.group), grid, tc::kThreads, gqa_tc_smem_bytes(), st, args);
 }
 
 }  // namespace dattn

@@ -2,6 +2,7 @@
 // CUDA kernels (dattn_kernels.cu) and the host engine (dattn_engine.cpp).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace dattn {
@@ -227,5 +228,25 @@ cudaError_t make_tmap_rows128(void* map_out, const void* base, uint64_t rows, ui
 cudaError_t launch_gqa_tc(const void* tm_k, const void* tm_v, const void* tm_q, const void* tm_k4,
                           const void* tm_v4, const MAParams& p, int grid, cudaStream_t st);
 cudaError_t launch_identity_records(int dtype, int dp, void* recs, int64_t n, cudaStream_t st);
+
+// Launch with programmatic stream serialization (PDL): the grid is scheduled
+// while the previous grid on the stream drains, and blocks in
+// griddepcontrol.wait until it has completed. The MA kernels use it behind the
+// previous step's merge grid (their set-up -- barriers, TMEM, tensor-map
+// prefetch -- overlaps its tail); DATTN_NO_PDL=1 turns it off (debug).
+inline cudaError_t launch_pdl_raw(const void* f, int grid, int block, size_t smem, cudaStream_t st, void** args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    static const bool off = std::getenv("DATTN_NO_PDL") != nullptr;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelExC(&cfg, f, args);
+}
 
 }  // namespace dattn

@@ -158,6 +158,10 @@ __global__ void __launch_bounds__(kMAThreads, (sizeof(T) == 8 || HPW > 1) ? 1 : 
     }
     if (threadIdx.x < kMergeQueue) mq.seq[threadIdx.x] = 0;
     __syncthreads();
+    // launched with programmatic serialization behind the previous step's
+    // merge grid: the set-up above overlapped its tail; records, q and the
+    // work counter are touched only after it has completed
+    pdl_wait();
 
     if (warp == kConsumerWarps + 1) {
         // ===================== merge warp (fused modes) =====================
@@ -563,6 +567,7 @@ __global__ void __launch_bounds__(32 * kGenericWarps) ma_generic_kernel(const MA
     constexpr int EPL = (DP + 31) / 32;
     constexpr int REC = DP + 4;
     pdl_launch_dependents();
+    pdl_wait();  // behind the previous step's merge grid (PDL launch)
     __shared__ int s_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const T* kpool = static_cast<const T*>(p.k_pool);
@@ -677,6 +682,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const MergePara
     __shared__ __align__(16) Acc s_acc[kMergeWarps][DP];
 
     pdl_wait();  // launched early behind the MA grid (PDL)
+    pdl_launch_dependents();  // the next step's MA grid may set up behind this one
     const int64_t g = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = static_cast<int>(g / p.heads);
@@ -801,6 +807,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_exchange_kernel(const 
     const Acc kNegInf = -static_cast<Acc>(INFINITY);
     const int64_t groups = static_cast<int64_t>(p.rows) * p.heads;
     pdl_wait();  // launched early behind the MA grid (PDL)
+    pdl_launch_dependents();  // the next step's MA grid may set up behind this one
     const Acc* R = static_cast<const Acc*>(p.recs);
     // DATTN_K5_TRACE: per-CTA sums over calls of (phase A done - start) and
     // (end - start), %globaltimer ns, and the call count
@@ -1297,7 +1304,12 @@ cudaError_t ma_generic_occupancy(int dtype, int dp, int* blocks_per_sm) {
 }
 
 cudaError_t launch_ma_generic(int dtype, int dp, const MAParams& p, int grid, cudaStream_t st) {
-    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (ma_generic_kernel<TC, DPC><<<grid, 32 * kGenericWarps, 0, st>>>(p))));
+    void* args[] = {const_cast<MAParams*>(&p)};
+    cudaError_t le = cudaSuccess;
+    DATTN_DT_SWITCH(dtype, DATTN_DP_SWITCH(dp, (le = launch_pdl_raw(reinterpret_cast<const void*>(
+                                                   ma_generic_kernel<TC, DPC>), grid, 32 * kGenericWarps, 0, st,
+                                               args))));
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 
@@ -1360,7 +1372,7 @@ cudaError_t launch_ma(int dtype, int dp, const MAParams& p, int grid, size_t sme
     const void* f = ma_kernel_ptr(dtype, dp, p.group);
     if (!f) return cudaErrorInvalidValue;
     void* args[] = {const_cast<MAParams*>(&p)};
-    return cudaLaunchKernel(f, dim3(grid), dim3(kMAThreads), args, smem, st);
+    return launch_pdl_raw(f, grid, kMAThreads, smem, st, args);
 }
 
 // launch with programmatic stream serialization: the kernel is scheduled
