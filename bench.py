@@ -379,6 +379,10 @@ def traffic_for(key: str):
 
 
 def run_b200_arm(args, rank, ws, local):
+    t_start = time.time()
+
+    def stage(name):
+        print(f"[bench rank {rank}] {name} (+{time.time() - t_start:.1f} s)", file=sys.stderr, flush=True)
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -463,6 +467,7 @@ def run_b200_arm(args, rank, ws, local):
     torch.cuda.synchronize()
     barrier()
 
+    stage("region A")
     # ---- region A: the headline, inputs resident in HBM ----
     sampler = ClockSampler(local)
     sampler.start()
@@ -483,6 +488,7 @@ def run_b200_arm(args, rank, ws, local):
     ms_step = ms_total / args.steps
     out_a = out.cpu()
 
+    stage("region B")
     # ---- region B: the MA kernel (K1/K2) alone, CUDA events around each launch on its stream ----
     st.stats(reset=True)
     st.set_timing(True)
@@ -501,6 +507,7 @@ def run_b200_arm(args, rank, ws, local):
         dist.all_gather_object(rank_times, [ma_ms, comm_ms])
     kernel_name = {1: "ma_decode_kernel (K1, CUDA cores)", 2: "gqa_tc_kernel (K2, tcgen05)"}.get(s.last_kernel, "?")
 
+    stage("region C")
     # ---- region C: static e2e (fixed batch) through the C ABI with host buffers ----
     qh = q.cpu().pin_memory()
     oh = torch.empty_like(qh).pin_memory()
@@ -513,6 +520,7 @@ def run_b200_arm(args, rank, ws, local):
     t_static = max_over_ranks(time.perf_counter() - t0) / ke
     static_same = bool(torch.equal(oh, out_a))
 
+    stage("region D")
     # ---- region D: the decode loop, end to end ----
     # inputs of every step, made before the region: the new token's K/V rows
     # (the generator's values at position L_r + t, so the oracle can check the
@@ -577,6 +585,7 @@ def run_b200_arm(args, rank, ws, local):
     qbytes = qh.numel() * qh.element_size()
     app_bytes = 2 * n_app * w.hkv * st.padded_dim * st.elem_bytes
 
+    stage("region E")
     # ---- region E (N > 1): paced block migration overlapped with decode ----
     # Every rank pulls m whole pages (K+V, all kv heads) of its left
     # neighbour's pool per decode step (dattn_kv_pull: copy engines over
@@ -593,12 +602,18 @@ def run_b200_arm(args, rank, ws, local):
         dist.all_gather_object(all_pages, my_pages)
         left = (rank + ws - 1) % ws
         src_pages = all_pages[left][:-1]  # full pages only (a sequence's last page may be partial)
+        # every rank runs the same rates (each step has collectives): the
+        # smallest source any rank pulls from bounds them
+        min_src = min(len(pg) - 1 for pg in all_pages)
         dst = st.seq_create(mig_cap * page)
         km = max(10, min(args.steps, 50))
         page_bytes = 2 * w.hkv * page * st.padded_dim * st.elem_bytes
         sweep = []
+        if min_src > 0:  # the first pull maps the peer pool lazily: keep it out of the sweep
+            st.kv_pull(dst, 0, left, src_pages[:1])
+            st.migration_join(wait_host=True)
         for m in [0] + mig_rates:
-            if m > len(src_pages):
+            if m > min_src:
                 continue
             pulls = [src_pages[(j * m) % (len(src_pages) - m + 1):][:m] for j in range(km + 3)]
 
@@ -669,6 +684,7 @@ def run_b200_arm(args, rank, ws, local):
                   "what": "bytes each rank pushes over NVLink per step in K5: one record per (row, q head) "
                           "to every peer, identity records only their 16-byte header"}
 
+    stage("parity")
     # ---- parity of what was timed (outside every timed region) ----
     parity = parity_loop = None
     if rank == 0 and not args.no_parity:
@@ -791,17 +807,29 @@ def main():
     if ws != args.gpus:
         print(f"[bench] refusing: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr, flush=True)
         return 2
+    # a rank stuck for BENCH_WATCHDOG_S seconds dumps every thread's stack
+    # to stderr and exits, instead of holding the box until an outer timeout
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("BENCH_WATCHDOG_S", "900")), exit=True)
     if ws > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     try:
-        return run_b200_arm(args, rank, ws, local)
-    finally:
-        if ws > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        rc = run_b200_arm(args, rank, ws, local)
+    except BaseException:
+        # the other ranks may sit in a collective: report and leave at once
+        # (torch.distributed.run then stops them) instead of blocking in
+        # destroy_process_group
+        import traceback
+        traceback.print_exc()
+        sys.stderr.flush()
+        os._exit(1)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
 
 
 if __name__ == "__main__":

@@ -102,6 +102,7 @@ void dattn_store::release_peer_pools() {
             if (peer_vpool[r]) cudaIpcCloseMemHandle(peer_vpool[r]);
         }
         peer_kpool[r] = peer_vpool[r] = nullptr;
+        peer_pages[r] = 0;
     }
     mig_pending = 0;
 }
@@ -119,27 +120,33 @@ void dattn_store::setup_peer_pools() {
         cuda_check(cudaStreamCreateWithPriority(&mig_stream, cudaStreamNonBlocking, lo), "cudaStreamCreate(mig)");
         cuda_check(cudaEventCreateWithFlags(&mig_ev, cudaEventDisableTiming), "cudaEventCreate(mig)");
     }
+    // per rank: K handle, V handle, pool size in pages
     constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+    constexpr size_t kRec = 2 * kH + sizeof(int64_t);
+    unsigned char rec[kRec];
     cudaIpcMemHandle_t h[2];
     cuda_check(cudaIpcGetMemHandle(&h[0], kpool), "cudaIpcGetMemHandle(k)");
     cuda_check(cudaIpcGetMemHandle(&h[1], vpool), "cudaIpcGetMemHandle(v)");
-    std::vector<unsigned char> all(2 * kH * nranks);
+    std::memcpy(rec, h, 2 * kH);
+    std::memcpy(rec + 2 * kH, &cfg.num_pages, sizeof(int64_t));
+    std::vector<unsigned char> all(kRec * nranks);
     DevBuf dh;
     dh.ensure(all.size());
-    unsigned char* mine = static_cast<unsigned char*>(dh.p) + rank * 2 * kH;
-    cuda_check(cudaMemcpyAsync(mine, h, 2 * kH, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync");
-    nccl_check(ncclAllGather(mine, dh.p, 2 * kH, ncclUint8, comm, comm_begin()), "ncclAllGather(pool handles)");
+    unsigned char* mine = static_cast<unsigned char*>(dh.p) + rank * kRec;
+    cuda_check(cudaMemcpyAsync(mine, rec, kRec, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync");
+    nccl_check(ncclAllGather(mine, dh.p, kRec, ncclUint8, comm, comm_begin()), "ncclAllGather(pool handles)");
     comm_end();
     cuda_check(cudaMemcpyAsync(all.data(), dh.p, all.size(), cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     for (int r = 0; r < nranks; ++r) {
+        std::memcpy(&peer_pages[r], all.data() + r * kRec + 2 * kH, sizeof(int64_t));
         if (r == rank) {
             peer_kpool[r] = kpool;
             peer_vpool[r] = vpool;
             continue;
         }
         cudaIpcMemHandle_t px[2];
-        std::memcpy(px, all.data() + r * 2 * kH, 2 * kH);
+        std::memcpy(px, all.data() + r * kRec, 2 * kH);
         cuda_check(cudaIpcOpenMemHandle(&peer_kpool[r], px[0], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(k)");
         cuda_check(cudaIpcOpenMemHandle(&peer_vpool[r], px[1], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(v)");
     }
@@ -1562,8 +1569,8 @@ dattn_status dattn_kv_pull(dattn_store* s, int32_t dst_seq, int64_t dst_tok0, in
         if (p0 + n_pages > s->seq_pages[dst_seq])
             throw Error(DATTN_ERR_CONTRACT, "destination pages outside the sequence");
         for (int64_t i = 0; i < n_pages; ++i)
-            if (src_pages[i] < 0 || src_pages[i] >= s->cfg.num_pages)
-                throw Error(DATTN_ERR_CONTRACT, "source page id out of range");
+            if (src_pages[i] < 0 || src_pages[i] >= s->peer_pages[src_rank])
+                throw Error(DATTN_ERR_CONTRACT, "source page id outside the source rank's pool");
         if (n_pages == 0) return;
         s->activate();
         // the destination pages' earlier writes (allocation, appends) come first

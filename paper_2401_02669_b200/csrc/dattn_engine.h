@@ -154,6 +154,7 @@ struct dattn_store {
     // low-priority stream beside the decode stream
     void* peer_kpool[8]{};
     void* peer_vpool[8]{};
+    int64_t peer_pages[8]{};  // pool size (pages) of every rank
     cudaStream_t mig_stream = nullptr;
     cudaEvent_t mig_ev = nullptr;
     int64_t mig_pending = 0;  // pulls issued since the last dattn_kv_migration_join

@@ -80,7 +80,6 @@ class ClusterDecodeLoop:
         appended on the rank that holds the slot, ledger advance. Returns the
         participants (stalled requests -- no block anywhere -- skip the step,
         ensure_step simengine.cpp:356-371)."""
-        import torch
         where = {r: self.led.ensure_slot(r, self.allow_borrow) for r in self.running}
         parts = [r for r in self.running if where[r] >= 0]
         self.stalled += len(self.running) - len(parts)
@@ -89,12 +88,8 @@ class ClusterDecodeLoop:
             for r in mine:
                 if r not in self.seqs:
                     self.seqs[r] = self.st.seq_create(0)  # first block hosted here
-            shape = (len(mine), self.st.num_kv_heads, self.st.padded_dim)
-            tdt = {BF16: torch.bfloat16, F32: torch.float32}.get(self.st.dtype, torch.float64)
             if self._kbuf is None or self._kbuf.shape[0] < len(mine):
-                dev = f"cuda:{self.st.device}"
-                self._kbuf = torch.empty(shape, dtype=tdt, device=dev)
-                self._vbuf = torch.empty(shape, dtype=tdt, device=dev)
+                self._kbuf, self._vbuf = self.row_buffers(len(mine))
             k, v = self._kbuf[: len(mine)], self._vbuf[: len(mine)]
             pos = [self.led.request(r)[1] for r in mine]
             self.st.synthetic_rows(mine, pos, self.seed, k, v, self.amp_k, self.amp_v)
@@ -102,6 +97,14 @@ class ClusterDecodeLoop:
         for r in parts:
             self.led.advance(r, 1)
         return parts
+
+    def row_buffers(self, n: int):
+        """Device buffers [n][num_kv_heads][padded_dim] for the new tokens' K/V rows."""
+        import torch
+        shape = (n, self.st.num_kv_heads, self.st.padded_dim)
+        tdt = {BF16: torch.bfloat16, F32: torch.float32}.get(self.st.dtype, torch.float64)
+        dev = f"cuda:{self.st.device}"
+        return torch.empty(shape, dtype=tdt, device=dev), torch.empty(shape, dtype=tdt, device=dev)
 
     def step(self, num_rows: int, q, out, mem: int = MEM_DEVICE) -> List[int]:
         """grow(), then the sharded decode over every rank's tokens."""
