@@ -85,6 +85,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="decode-loop steps (0: min(--steps, 64))")
     ap.add_argument("--chunk-tokens", type=int, default=0)
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check (profiling runs)")
+    ap.add_argument("--no-overflow-loop", action="store_true", help="N>1: skip the overflow-borrowing decode loop")
+    ap.add_argument("--overflow-steps", type=int, default=48)
     ap.add_argument("--migration-pages", default="1,16,128,512",
                     help="N>1: pages pulled per decode step in the migration-overlap sweep ('' skips it)")
     return ap.parse_args()
@@ -684,6 +686,68 @@ def run_b200_arm(args, rank, ws, local):
                   "what": "bytes each rank pushes over NVLink per step in K5: one record per (row, q head) "
                           "to every peer, identity records only their 16-byte header"}
 
+    stage("region G")
+    # ---- region G (N > 1): decode loop whose KV outgrows its home GPU ----
+    # The same batch with every request homed whole on one GPU (round robin),
+    # each GPU's page pool sized to its requests plus headroom -- none on
+    # GPU 0. As contexts grow, GPU 0's requests take their next blocks on
+    # peers through the block ledger's ensure_slot (simengine.cpp:318-354,
+    # dattn_ledger_*): the slot's GPU appends the token, every GPU decodes the
+    # tokens it holds (decode_loop.ClusterDecodeLoop). Host clock per step
+    # (slot decisions + append + sharded decode, synchronised), max over ranks;
+    # parity of the last step against the oracle at the grown lengths.
+    overflow = None
+    if ws > 1 and not args.no_overflow_loop:
+        from paper_2401_02669_b200.decode_loop import ClusterDecodeLoop
+        kg = args.overflow_steps
+        homes = [i % ws for i in range(w.batch)]
+        need = [0] * ws
+        for i, L in enumerate(w.lens):
+            need[homes[i]] += pb.blocks_for_tokens(L, page)
+        n0 = sum(1 for h in homes if h == 0)
+        grow_blocks = -(-kg // page) + 1
+        caps = [need[0]] + [need[r] + 2 * (w.batch // ws + n0) * grow_blocks for r in range(1, ws)]
+        st2 = pb.Store(w.d, w.hq, w.hkv, w.dtype, page, caps[rank], max_seqs=w.batch + 4,
+                       max_pages_per_seq=max(caps), device=local)
+        st2.set_stream(stream.cuda_stream)
+        uid2 = [pb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid2, src=0)
+        st2.comm_init(uid2[0], rank, ws)
+        loop = ClusterDecodeLoop(st2, rank, ws, caps, w.seed, w.amp_k, w.amp_v)
+        for i, L in enumerate(w.lens):
+            assert loop.admit(i, i, L, home=homes[i])
+        out2 = torch.empty_like(q)
+        for _ in range(3):
+            loop.step(w.batch, q, out2)
+        torch.cuda.synchronize()
+        barrier()
+        per = []
+        t0 = time.perf_counter()
+        for _ in range(kg):
+            c = time.perf_counter()
+            loop.step(w.batch, q, out2)
+            torch.cuda.synchronize()
+            per.append(time.perf_counter() - c)
+        t_g = max_over_ranks(time.perf_counter() - t0) / kg
+        lens_g = [loop.led.request(i)[1] for i in range(w.batch)]
+        pages_ok = st2.info().free_pages == loop.led.free_blocks(rank)
+        oks2 = [None] * ws
+        dist.all_gather_object(oks2, pages_ok)
+        par_g = None
+        if rank == 0 and not args.no_parity:
+            par_g = parity_check(w, out2.float().cpu().numpy() if w.dtype == 0 else out2.cpu().numpy(), lens_g)
+        hosted = sum(1 for i in range(w.batch) if len({s_[0] for s_ in loop.led.segments(i)}) > 1)
+        per.sort()
+        overflow = {"what": "decode loop, requests homed whole round robin, GPU 0's pool without headroom: its "
+                            "requests borrow blocks on peers (ensure_slot) as they grow; host clock per step incl. "
+                            "slot decisions, appends and the sharded decode (synchronised), max over ranks",
+                    "ms_per_step": t_g * 1e3, "tokens_per_s": w.batch / t_g, "steps": kg,
+                    "step_ms_rank0": {"median": 1e3 * per[len(per) // 2], "max": 1e3 * per[-1]},
+                    "capacity_blocks": caps, "borrowed_blocks": loop.led.borrowed(),
+                    "requests_spanning_gpus": hosted, "stalled_request_steps": loop.stalled,
+                    "pages_equal_ledger_per_rank": oks2, "parity": par_g}
+        st2.close()
+
     stage("parity")
     # ---- parity of what was timed (outside every timed region) ----
     parity = parity_loop = None
@@ -754,6 +818,8 @@ def run_b200_arm(args, rank, ws, local):
         line["nvlink"] = nvlink
     if migration:
         line["migration"] = migration
+    if overflow:
+        line["overflow_decode_loop"] = overflow
     if ws == 1 and not args.no_cpu_baseline:
         cv, info = cpu_reference_sample(w, args.cpu_seconds)
         c1, info1 = cpu_reference_sample(w, min(args.cpu_seconds, 4.0), threads=1)
@@ -763,7 +829,7 @@ def run_b200_arm(args, rank, ws, local):
                                 "single_thread_value": c1, "single_thread_reps": info1["reps"],
                                 "kv_gbs_fp64": info["kv_gbs_fp64"], "single_thread_kv_gbs_fp64": info1["kv_gbs_fp64"]}
     emit(line)
-    ok = all(p is None or p["pass"] for p in (parity, parity_loop))
+    ok = all(p is None or p["pass"] for p in (parity, parity_loop, (overflow or {}).get("parity")))
     if not ok:
         print("[bench] PARITY FAILED: " + json.dumps({"parity": parity, "parity_decode_loop": parity_loop}),
               file=sys.stderr, flush=True)
