@@ -165,6 +165,8 @@ _FUNCS = {
     "dattn_ledger_admit": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]),
     "dattn_ledger_ensure_slot": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     "dattn_ledger_advance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64]),
+    "dattn_ledger_step": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                         ctypes.c_void_p]),
     "dattn_ledger_release": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "dattn_ledger_instance": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "dattn_ledger_request": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
@@ -533,6 +535,15 @@ class Ledger:
 
     def advance(self, req: int, tokens: int = 1):
         check(lib.dattn_ledger_advance(self._h, req, tokens))
+
+    def step(self, reqs: Sequence[int], allow_borrow: bool = True):
+        """ensure_slot for every request in order, then advance those with a
+        slot by one token; returns the slot instances (-1: stalled)."""
+        n = len(reqs)
+        ra = (ctypes.c_int64 * max(n, 1))(*reqs)
+        out = (ctypes.c_int * max(n, 1))()
+        check(lib.dattn_ledger_step(self._h, n, ra, 1 if allow_borrow else 0, out))
+        return list(out[:n])
 
     def release(self, req: int) -> int:
         f = ctypes.c_int64()

@@ -466,7 +466,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
         throw Error(DATTN_ERR_INVALID_ARGUMENT, "negative row/range count");
     if (b.num_ranges > 0 && !b.ranges)
         throw Error(DATTN_ERR_INVALID_ARGUMENT, "ranges is null");
-    const int nr = b.num_ranges;
+    int nr = b.num_ranges;
     int64_t work = 0, max_len = 0;
     int prev_row = -1;
     for (int i = 0; i < nr; ++i) {
@@ -508,6 +508,57 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     if (C > INT32_MAX) throw Error(DATTN_ERR_CONTRACT, "chunk too long");
     pl.chunk_tokens = static_cast<int32_t>(C);
 
+    // Fine tail for uniform batches: when every range is a whole number of
+    // full chunks, the last wave of items would be full chunks too and the
+    // grid would drain over one chunk's streaming time. The trailing chunks
+    // of some ranges are then cut into sub-ranges of C/4 tokens (partial
+    // chunks), which the longest-first claim order below runs last: about two
+    // waves of quarter items end the launch. Same records and merges; only
+    // the chunk boundaries move (partition invariance).
+    const dattn_range* R = b.ranges;
+    std::vector<dattn_range> split;
+    // K2 runs one CTA per SM; quarter chunks below 1K tokens cost more per
+    // item than the shorter drain saves (measured: config 3 at N = 4, C = 2048:
+    // +2.4 us per step; C = 4096 / 8192: -8 / -17 us)
+    const int64_t slots = static_cast<int64_t>(num_sms) * (tc_ok ? 1 : ma_ctas_per_sm);
+    static const bool fine_tail_off = std::getenv("DATTN_NO_FINE_TAIL") != nullptr;  // A/B switch
+    if (!fine_tail_off && !one_chunk_per_range && b.chunk_tokens <= 0 && C >= 4096 &&
+        C % (4 * cfg.page_tokens) == 0) {
+        bool uniform = nr > 0;
+        int64_t nh_sum = 0, natural = 0;
+        for (int i = 0; i < nr && uniform; ++i) {
+            const int64_t len = R[i].tok_end - R[i].tok_begin;
+            if (len > 0 && (len % C != 0 || len < 2 * C)) uniform = false;
+            const int nh = R[i].kv_head < 0 ? cfg.num_kv_heads : 1;
+            if (len > 0) nh_sum += nh;
+            natural += len / C * nh;
+        }
+        // only when there is a last wave to shorten (at least two waves of items)
+        if (uniform && nh_sum > 0 && natural >= 2 * slots) {
+            const int64_t want = 2 * slots;  // quarter items wanted
+            // chunks to cut per range (round robin over the ranges, at most
+            // all but one of a range's chunks)
+            const int64_t per_range = std::max<int64_t>(1, (want + 4 * nh_sum - 1) / (4 * nh_sum));
+            split.reserve(static_cast<size_t>(nr) * (1 + 4 * per_range));
+            const int64_t q = C / 4;
+            for (int i = 0; i < nr; ++i) {
+                dattn_range r = R[i];
+                const int64_t len = r.tok_end - r.tok_begin;
+                const int64_t k = len > 0 ? std::min(per_range, len / C - 1) : 0;
+                r.tok_end = R[i].tok_end - k * C;
+                split.push_back(r);
+                for (int64_t j = 0; j < 4 * k; ++j) {
+                    dattn_range s2 = R[i];
+                    s2.tok_begin = r.tok_end + j * q;
+                    s2.tok_end = s2.tok_begin + q;
+                    split.push_back(s2);
+                }
+            }
+            R = split.data();
+            nr = static_cast<int>(split.size());
+        }
+    }
+
     // layout of the metadata buffer (int32 words)
     pl.off_ranges = 0;
     pl.off_item = pl.off_ranges + 8 * nr;
@@ -519,7 +570,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     int64_t items = 0, chunks = 0;
     std::vector<int32_t> row_chunks(b.num_rows, 0);
     for (int i = 0; i < nr; ++i) {
-        const dattn_range& r = b.ranges[i];
+        const dattn_range& r = R[i];
         const int64_t len = r.tok_end - r.tok_begin;
         const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
         const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
@@ -545,7 +596,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     bool any_kvh = false;
     int64_t c = 0;
     for (int i = 0; i < nr; ++i) {
-        const dattn_range& r = b.ranges[i];
+        const dattn_range& r = R[i];
         const int64_t len = r.tok_end - r.tok_begin;
         const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
         for (int64_t k = 0; k < nch; ++k) pl.words[pl.off_kvh + c++] = r.kv_head;
@@ -556,7 +607,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     pl.off_expect = pl.words.size();
     pl.words.resize(pl.off_expect + static_cast<size_t>(b.num_rows) * cfg.num_kv_heads, 0);
     for (int i = 0; i < nr; ++i) {
-        const dattn_range& r = b.ranges[i];
+        const dattn_range& r = R[i];
         const int64_t len = r.tok_end - r.tok_begin;
         const int64_t nch = len > 0 ? (len + C - 1) / C : 0;
         int32_t* e = &pl.words[pl.off_expect + static_cast<size_t>(r.out_row) * cfg.num_kv_heads];
@@ -582,7 +633,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
         std::vector<Tail> tails;  // ranges whose last chunk is shorter than C
         int32_t lmin = INT32_MAX, lmax = 0;
         for (int i = 0; i < nr; ++i) {
-            const dattn_range& r = b.ranges[i];
+            const dattn_range& r = R[i];
             const int64_t len = r.tok_end - r.tok_begin;
             if (len <= 0) continue;
             const int32_t last = static_cast<int32_t>(len - (len - 1) / C * C);
@@ -598,7 +649,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
             int32_t* tab = &pl.words[pl.off_table];
             size_t k = 0;
             for (int i = 0; i < nr; ++i) {  // full chunks, natural order
-                const dattn_range& r = b.ranges[i];
+                const dattn_range& r = R[i];
                 const int64_t len = r.tok_end - r.tok_begin;
                 if (len <= 0) continue;
                 const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
@@ -610,7 +661,7 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
                 }
             }
             for (const Tail& t : tails) {  // partial last chunks, longest first
-                const dattn_range& r = b.ranges[t.range];
+                const dattn_range& r = R[t.range];
                 const int nh = r.kv_head < 0 ? cfg.num_kv_heads : 1;
                 const int64_t j = (r.tok_end - r.tok_begin - 1) / C;
                 for (int h = 0; h < nh; ++h) {

@@ -212,6 +212,16 @@ dattn_status dattn_ledger_advance(dattn_ledger* l, int64_t req, int64_t tokens) 
     });
 }
 
+dattn_status dattn_ledger_step(dattn_ledger* l, int n, const int64_t* reqs, int allow_borrow, int* instances) {
+    return guarded([&] {
+        REQUIRE_ARG(l && (n == 0 || (reqs && instances)), "null argument");
+        if (n < 0) throw Error(DATTN_ERR_CONTRACT, "ledger: negative request count");
+        for (int i = 0; i < n; ++i) instances[i] = l->ensure_slot(reqs[i], allow_borrow != 0);
+        for (int i = 0; i < n; ++i)
+            if (instances[i] >= 0) l->req(reqs[i]).ctx += 1;
+    });
+}
+
 dattn_status dattn_ledger_release(dattn_ledger* l, int64_t req, int64_t* freed_blocks) {
     return guarded([&] {
         REQUIRE_ARG(l, "null argument");

@@ -38,6 +38,8 @@ class ClusterDecodeLoop:
         self.seed, self.amp_k, self.amp_v = seed, amp_k, amp_v
         self.allow_borrow = allow_borrow
         self.seqs: Dict[int, int] = {}  # request -> this rank's sequence (home or hosted)
+        self.local: Dict[int, int] = {}  # request -> tokens of it this rank holds (= its segments here)
+        self.ctx: Dict[int, int] = {}  # request -> context length (= the ledger's)
         self.rows: Dict[int, int] = {}  # request -> output row
         self.running: List[int] = []  # admission order, like the simulator's running list
         self.stalled = 0
@@ -56,14 +58,18 @@ class ClusterDecodeLoop:
         if not self.led.admit(req, home, tokens):
             return False
         self.rows[req] = row
+        self.ctx[req] = tokens
         self.running.append(req)
         if home == self.rank:
             s = self.st.seq_create(tokens)
             self.st.fill_synthetic(s, self.seed, req, 0, self.amp_k, self.amp_v)
             self.seqs[req] = s
+            self.local[req] = tokens
         return True
 
     def local_tokens(self, req: int) -> int:
+        """Tokens of req on this rank, from the ledger's segments (the loop
+        keeps the same count incrementally in self.local)."""
         return sum(hi - lo for inst, lo, hi in self.led.segments(req) if inst == self.rank)
 
     def ranges(self) -> List[Range]:
@@ -71,7 +77,7 @@ class ClusterDecodeLoop:
         requests it holds nothing of)."""
         out = []
         for r in sorted(self.running, key=lambda r: self.rows[r]):
-            n = self.local_tokens(r) if r in self.seqs else 0
+            n = self.local.get(r, 0)
             out.append(Range(self.seqs[r] if n else self._none, self.rows[r], 0, n))
         return out
 
@@ -80,7 +86,8 @@ class ClusterDecodeLoop:
         appended on the rank that holds the slot, ledger advance. Returns the
         participants (stalled requests -- no block anywhere -- skip the step,
         ensure_step simengine.cpp:356-371)."""
-        where = {r: self.led.ensure_slot(r, self.allow_borrow) for r in self.running}
+        inst = self.led.step(self.running, self.allow_borrow)  # ensure_slot + advance, one call
+        where = dict(zip(self.running, inst))
         parts = [r for r in self.running if where[r] >= 0]
         self.stalled += len(self.running) - len(parts)
         mine = [r for r in parts if where[r] == self.rank]
@@ -91,11 +98,13 @@ class ClusterDecodeLoop:
             if self._kbuf is None or self._kbuf.shape[0] < len(mine):
                 self._kbuf, self._vbuf = self.row_buffers(len(mine))
             k, v = self._kbuf[: len(mine)], self._vbuf[: len(mine)]
-            pos = [self.led.request(r)[1] for r in mine]
-            self.st.synthetic_rows(mine, pos, self.seed, k, v, self.amp_k, self.amp_v)
+            # a new token's position is its request's context length before the step
+            self.st.synthetic_rows(mine, [self.ctx[r] for r in mine], self.seed, k, v, self.amp_k, self.amp_v)
             self.st.kv_append([self.seqs[r] for r in mine], k, v, mem=MEM_DEVICE)
+            for r in mine:
+                self.local[r] = self.local.get(r, 0) + 1
         for r in parts:
-            self.led.advance(r, 1)
+            self.ctx[r] += 1
         return parts
 
     def row_buffers(self, n: int):
@@ -116,6 +125,8 @@ class ClusterDecodeLoop:
         """complete (simengine.cpp:300-303): free_request everywhere."""
         self.led.release(req)
         self.running.remove(req)
+        self.local.pop(req, None)
+        self.ctx.pop(req, None)
         s = self.seqs.pop(req, None)
         if s is not None:
             self.st.seq_release(s)

@@ -47,15 +47,25 @@ static void run(const char* name, dattn_store* s, const std::vector<dattn_range>
     const int C = pl.chunk_tokens;
     std::string js = std::string("{\"name\": \"") + name + "\", \"chunk\": " + std::to_string(C) +
                      ", \"items\": " + std::to_string(pl.nitems) + ", \"chunks\": " + std::to_string(pl.nchunks) +
-                     ", \"table\": " + (pl.off_table ? "true" : "false");
+                     ", \"table\": " + (pl.off_table ? "true" : "false") + ", \"nranges\": " + std::to_string(nr);
+    js += ", \"ranges\": [";
+    for (int r = 0; r < nr; ++r) {
+        const int32_t* rg = &pl.words[pl.off_ranges + 8 * r];
+        js += (r ? ", [" : "[") + std::to_string(rg[0]) + ", " + std::to_string(rg[1]) + ", " + std::to_string(rg[2]) +
+              ", " + std::to_string(rg[3]) + ", " + std::to_string(rg[4]) + "]";
+    }
+    js += "]";
     // item lengths in claim order
+    // the plan's own ranges (the builder may cut trailing chunks of uniform
+    // batches into sub-ranges): RangeDev {seq, out_row, kv_head, lo, hi, pad[3]}
     auto item_len = [&](int r, int local) {
-        const dattn_range& rg = rs[r];
-        const int nh = rg.kv_head < 0 ? s->cfg.num_kv_heads : 1;
+        const int32_t* rg = &pl.words[pl.off_ranges + 8 * r];
+        const int nh = rg[2] < 0 ? s->cfg.num_kv_heads : 1;
         const int j = local / nh;
-        const int64_t lo = rg.tok_begin + static_cast<int64_t>(j) * C;
-        return static_cast<int64_t>(std::min<int64_t>(rg.tok_end, lo + C) - lo);
+        const int64_t lo = rg[3] + static_cast<int64_t>(j) * C;
+        return static_cast<int64_t>(std::min<int64_t>(rg[4], lo + C) - lo);
     };
+    (void)rs;
     js += ", \"order\": [";
     for (int k = 0; k < pl.nitems; ++k) {
         int r, local;
@@ -99,7 +109,8 @@ int main() {
         run("ragged_k2", s, rs, 8);
         delete s;
     }
-    {  // equal lengths (config-3 like): natural order, no table
+    {  // equal lengths (config-3 like): full chunks in natural order, then the
+       // trailing chunks cut into quarter sub-ranges, run last
         auto* s = make_store(64, 8, 0, 20, true, 1);
         std::vector<dattn_range> rs;
         for (int i = 0; i < 16; ++i) rs.push_back(R(i, i, 0, 131072));

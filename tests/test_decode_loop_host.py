@@ -69,6 +69,9 @@ def run(world, caps, prompts, steps, seed):
         assert all(p == parts[0] for p in parts)  # replicas agree
         for r in range(world):
             assert stores[r].used() == caps[r] - loops[r].led.free_blocks(r)
+            for req in loops[r].running:  # the loop's incremental counts = the ledger's segments
+                assert loops[r].local.get(req, 0) == loops[r].local_tokens(req)
+                assert loops[r].ctx[req] == loops[r].led.request(req)[1]
         for req in loops[0].running:
             ctx = loops[0].led.request(req)[1]
             held = []

@@ -235,3 +235,27 @@ def test_segments_partition_the_context():
                     used[i] += led.blocks(r, i)
                 assert sum(led.blocks(r, i) for i in range(4)) == held
             assert used == [led.instance(i)[1] for i in range(4)]
+
+
+def test_batched_step_equals_slot_then_advance():
+    """dattn_ledger_step (one call per decode step) = ensure_slot for every
+    request in order, then advance the ones that got a slot."""
+    rng = random.Random(21)
+    caps = [20, 14, 30]
+    a, b = pb.Ledger(caps, 16), pb.Ledger(caps, 16)
+    reqs = []
+    for i in range(7):
+        L = rng.randint(1, 120)
+        h = rng.randrange(3)
+        if a.admit(i, h, L):
+            assert b.admit(i, h, L)
+            reqs.append(i)
+    for _ in range(200):
+        got = a.step(reqs)
+        want = [b.ensure_slot(r) for r in reqs]
+        for r, w in zip(reqs, want):
+            if w >= 0:
+                b.advance(r)
+        assert got == want
+    assert [a.segments(r) for r in reqs] == [b.segments(r) for r in reqs]
+    assert [a.instance(j) for j in range(3)] == [b.instance(j) for j in range(3)]

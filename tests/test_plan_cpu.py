@@ -55,11 +55,28 @@ def test_ragged_batch_claims_longest_first(plans):
     assert p["expect"] == [math.ceil(L / C) for L in lens for _ in range(32)]
 
 
-def test_uniform_batch_keeps_natural_order(plans):
+def test_uniform_batch_ends_on_quarter_chunks(plans):
+    """Equal lengths: full chunks claimed in natural order (kv heads of a chunk
+    adjacent), then each range's last chunk cut into four C/4 sub-ranges that
+    run last, so the launch drains over a quarter chunk, not a full one; the
+    sub-ranges tile the range exactly (partition invariance)."""
     p = plans["uniform_k2"]
-    assert p["chunk"] == 8192 and not p["table"]
-    assert [i for i, _ in p["order"]] == list(range(p["items"]))
-    assert p["items"] == 16 * (131072 // 8192) * 8
+    C = p["chunk"]
+    assert C == 8192 and p["table"]
+    per_range = 131072 // C  # 16 chunks per request
+    full = 16 * (per_range - 1) * 8
+    assert p["items"] == full + 16 * 4 * 8
+    order = p["order"]
+    assert [t for _, t in order[:full]] == [C] * full
+    assert [i for i, _ in order[:full]] == sorted(i for i, _ in order[:full])
+    assert [t for _, t in order[full:]] == [C // 4] * (16 * 4 * 8)
+    assert sorted(i for i, _ in order) == list(range(p["items"]))
+    for req in range(16):  # every request still covered exactly once, in order
+        spans = [(lo, hi) for seq, row, kvh, lo, hi in p["ranges"] if row == req]
+        assert spans[0][0] == 0 and spans[-1][1] == 131072
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert p["row_chunks"] == [per_range - 1 + 4] * 16
+    assert p["expect"] == [per_range - 1 + 4] * (16 * 8)
 
 
 def test_small_fp32_batch_uses_the_chunk_floor(plans):
