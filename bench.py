@@ -48,6 +48,7 @@ it never loads the product library.
 from __future__ import annotations
 
 import argparse
+import gc
 import hashlib
 import json
 import os
@@ -470,6 +471,10 @@ def run_b200_arm(args, rank, ws, local):
     barrier()
 
     stage("region A")
+    # no Python garbage collection inside the timed regions: a gen-2 pass over
+    # torch's heap stalled one decode-loop step for ~0.5 s (r2z run)
+    gc.collect()
+    gc.disable()
     # ---- region A: the headline, inputs resident in HBM ----
     sampler = ClockSampler(local)
     sampler.start()
@@ -748,6 +753,7 @@ def run_b200_arm(args, rank, ws, local):
                     "pages_equal_ledger_per_rank": oks2, "parity": par_g}
         st2.close()
 
+    gc.enable()
     stage("parity")
     # ---- parity of what was timed (outside every timed region) ----
     parity = parity_loop = None
