@@ -549,6 +549,7 @@ def run_b200_arm(args, rank, ws, local):
     cur_end = [rr.tokens for rr in shares]
 
     brk = [0.0, 0.0, 0.0]  # host seconds in append / range build / decode call
+    split_log = []  # per step: (t, append ms, range build ms, decode call ms)
 
     def loop_step(t):
         c0 = time.perf_counter()
@@ -572,6 +573,7 @@ def run_b200_arm(args, rank, ws, local):
         brk[0] += c1 - c0
         brk[1] += c2 - c1
         brk[2] += c3 - c2
+        split_log.append((t, 1e3 * (c1 - c0), 1e3 * (c2 - c1), 1e3 * (c3 - c2)))
 
     for t in range(3):  # warm-up steps grow the contexts too
         loop_step(t)
@@ -585,6 +587,7 @@ def run_b200_arm(args, rank, ws, local):
         loop_step(t)
         per_step.append(time.perf_counter() - c)
     t_loop = max_over_ranks(time.perf_counter() - t0) / ke
+    slowest = sorted(split_log[3:], key=lambda x: -(x[1] + x[2] + x[3]))[:3]
     per_step.sort()
     plan_bytes = st.stats().last_plan_bytes
     lens_now = [L + grow_total for L in w.lens]
@@ -807,7 +810,9 @@ def run_b200_arm(args, rank, ws, local):
                 "host_ms_rank0": {"kv_append_call": 1e3 * brk[0] / ke, "range_build": 1e3 * brk[1] / ke,
                                   "decode_call": 1e3 * brk[2] / ke},
                 "step_ms_rank0": {"median": 1e3 * per_step[len(per_step) // 2],
-                                  "p90": 1e3 * per_step[int(0.9 * (len(per_step) - 1))], "max": 1e3 * per_step[-1]}},
+                                  "p90": 1e3 * per_step[int(0.9 * (len(per_step) - 1))], "max": 1e3 * per_step[-1],
+                                  "slowest": [{"step": t_, "append_ms": round(a_, 3), "ranges_ms": round(b_, 3),
+                                               "decode_call_ms": round(c_, 3)} for t_, a_, b_, c_ in slowest]}},
         "e2e_static": {"value": w.batch / t_static, "unit": "tokens/s", "ms_per_step": t_static * 1e3,
                        "h2d_bytes_per_step": qbytes, "d2h_bytes_per_step": qbytes,
                        "what": "fixed batch repeated (plan cached), H2D q + D2H output"},
