@@ -363,21 +363,54 @@ def parity_check(w, out_host, lens, budget_tok_heads: float = 4e6):
 
 # ----------------------------------------------------------------- GPU side
 
+def kernel_code_sha256(lib_path: str):
+    """sha256 over the device code of a library: the .text.* (SASS) and
+    .nv.info* sections of every cubin embedded in it (cuobjdump -xelf all).
+    nvcc builds are not byte-reproducible -- the fatbin and the cubins' debug
+    line tables carry per-build temporary names -- but this code hash is, so a
+    capture stays valid across rebuilds of the same sources and nothing else."""
+    import struct
+    with tempfile.TemporaryDirectory() as td:
+        r = subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib_path)], cwd=td,
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            return None
+        h = hashlib.sha256()
+        for fn in sorted(os.listdir(td)):
+            b = open(os.path.join(td, fn), "rb").read()
+            if b[:4] != b"\x7fELF" or b[4] != 2:
+                continue
+            shoff, = struct.unpack_from("<Q", b, 0x28)
+            shentsize, shnum, shstrndx = struct.unpack_from("<HHH", b, 0x3A)
+            secs = [struct.unpack_from("<IIQQQQIIQQ", b, shoff + i * shentsize) for i in range(shnum)]
+            stro = secs[shstrndx][4]
+
+            def name(off):
+                e = b.index(b"\0", stro + off)
+                return b[stro + off:e].decode()
+            for sh in sorted(secs, key=lambda x: name(x[0])):
+                nm = name(sh[0])
+                if nm.startswith(".text.") or nm.startswith(".nv.info"):
+                    h.update(fn.encode() + nm.encode() + b[sh[4]:sh[4] + sh[5]])
+        return h.hexdigest()
+
+
 def traffic_for(key: str):
     """DRAM bytes per launch of the dominant kernel from profiles/ncu_traffic.json,
-    only when that capture was made on this exact library build."""
+    only when that capture was made on this library's device code (same
+    kernel_code_sha256; the whole-file hash of a rebuild differs)."""
     import paper_2401_02669_b200 as pb
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         j = json.load(open(tf))
         ent = j.get(key)
-        sha = hashlib.sha256(open(pb.LIB_PATH, "rb").read()).hexdigest()
     except Exception:
         return None, "no capture"
     if not isinstance(ent, dict):
         return None, "no capture for this config"
-    if ent.get("lib_sha256") != sha:
-        return None, f"capture of another build ({ent.get('git_head', '?')}); not reported"
+    code = kernel_code_sha256(pb.LIB_PATH)
+    if code is None or ent.get("code_sha256") != code:
+        return None, f"capture of other device code ({ent.get('git_head', '?')}); not reported"
     return ent.get("traffic"), f"ncu --set full, {ent.get('kernel')}, build {ent.get('git_head', '?')}"
 
 

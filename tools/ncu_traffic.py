@@ -3,7 +3,9 @@
 report into profiles/ncu_traffic.json, stamped with the library build it was
 measured on (sha256 of paper_2401_02669_b200/_lib/libdattn.so) and the git
 head. bench.py reports ``roofline.traffic`` only when the stamp matches the
-library it runs, so a capture of an older build can never feed a bench line.
+library it runs (compared by the hash of its device code, which survives a
+rebuild of the same sources), so a capture of other kernel code can never feed
+a bench line.
 
     python tools/ncu_traffic.py KEY REPORT.ncu-rep [--kernel REGEX]
 
@@ -20,6 +22,7 @@ import json
 import os
 import re
 import subprocess
+import sys
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,6 +44,10 @@ def launches(rep: str):
 def num(cell) -> float:
     v, u = cell
     return float(v.replace(",", "")) * UNIT.get(u, 1)
+
+
+sys.path.insert(0, ROOT)
+from bench import kernel_code_sha256  # noqa: E402
 
 
 def main():
@@ -68,6 +75,7 @@ def main():
     j[a.key] = {"traffic": sum(tr) / len(tr), "launches": len(tr), "kernel": sorted(names)[0],
                 "duration_ns": sum(dur) / len(dur) if dur else None,
                 "lib_sha256": hashlib.sha256(open(LIB, "rb").read()).hexdigest(),
+                "code_sha256": kernel_code_sha256(LIB),
                 "git_head": head, "report": os.path.basename(a.report),
                 "recorded": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
                 "metric": "dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)"}
