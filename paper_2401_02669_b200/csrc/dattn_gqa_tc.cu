@@ -14,9 +14,9 @@
 // MMA1 and the MN-major A operand of MMA2. P^T is written by the softmax
 // warps in the same swizzled K-major layout.
 //
-// Warp roles (192 threads): w0 TMA producer, w1 TMEM owner + single-thread
-// MMA issuer, w2..w5 softmax / epilogue (thread = token row of S^T, then
-// d row of O^T). Online softmax: per-tile max across the 128 tokens through
+// Warp roles (256 threads): w0 K producer, w1 TMEM owner + single-thread MMA
+// issuer, w2..w5 softmax / epilogue (thread = token row of S^T, then d row of
+// O^T), w6 V producer, w7 merge (fused modes). Online softmax: per-tile max via
 // shared memory, P rounded to bf16 (the same value enters e and the P.V
 // MMA), the O^T tile rescale-accumulated in registers.
 #include <cuda.h>
