@@ -492,9 +492,13 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     } else if (b.chunk_tokens > 0) {
         C = b.chunk_tokens;
     } else {
-        // ~12 items per CTA for K1; ~6 for K2, whose items cost a pipeline
-        // drain each (measured: 2048-token chunks 2-3% slower than 4096 at the
-        // same wave count, 1024-token chunks 8%)
+        // ~12 items per CTA slot for K1 and ~6 for K2 (whose items cost a
+        // pipeline drain each: 2048-token chunks 2-3% slower than 4096 at the
+        // same wave count, 1024-token chunks 8%). ma_ctas_per_sm is K1's
+        // occupancy (2 for bf16), so K2 -- one CTA per SM -- gets ~12 items per
+        // SM: measured better than ~6 at N = 4 (config 3: 0.313 vs 0.320 ms per
+        // rank with 2048- vs 4096-token chunks; config 4: 0.585 vs 0.620 with
+        // 4096 vs 8192), where the shares are small and the tail matters more
         const int64_t target = static_cast<int64_t>(num_sms) * ma_ctas_per_sm * (tc_ok ? 6 : 12);
         int64_t c = std::max<int64_t>(work / std::max<int64_t>(target, 1), 1);
         int64_t p2 = 1;
