@@ -582,6 +582,24 @@ def run_b200_arm(args, rank, ws, local):
     cur_end = [rr.tokens for rr in shares]
 
     brk = [0.0, 0.0, 0.0]  # host seconds in append / range build / decode call
+    # the decode loop's ranges, packed once: the last range of every request
+    # (the one that grows) is tok_end-updated in place through a numpy view
+    loop_rg, grow_idx = [], []
+    for i, rr in enumerate(shares):
+        if ws > 1 or w.rblocks == 1:
+            loop_rg.append(pb.Range(seqs[i], rr.request, 0, rr.tokens))
+        else:
+            cuts = [rr.tokens * j // w.rblocks for j in range(w.rblocks + 1)]
+            loop_rg.extend(pb.Range(seqs[i], rr.request, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
+        grow_idx.append(len(loop_rg) - 1)
+    loop_ra = pb.range_array(loop_rg)
+    loop_view = np.ctypeslib.as_array(loop_ra.arr)
+    grow_idx = np.asarray(grow_idx)
+
+    class _Ends:  # loop_ends[:] = cur_end writes tok_end of the growing ranges
+        def __setitem__(self, key, vals):
+            loop_view["tok_end"][grow_idx] = vals
+    loop_ends = _Ends()
     split_log = []  # per step: (t, append ms, range build ms, decode call ms)
 
     def loop_step(t):
@@ -592,16 +610,11 @@ def run_b200_arm(args, rank, ws, local):
                 cur_end[i] += 1
         c1 = time.perf_counter()
         # every range of a request ends at its current length (ws > 1: one
-        # range per request per rank; ws == 1: rBlock cuts, the last one grows)
-        rg = []
-        for i, rr in enumerate(shares):
-            if ws > 1 or w.rblocks == 1:
-                rg.append(pb.Range(seqs[i], rr.request, 0, cur_end[i]))
-            else:
-                cuts = [rr.tokens * j // w.rblocks for j in range(w.rblocks)] + [cur_end[i]]
-                rg.extend(pb.Range(seqs[i], rr.request, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
+        # range per request per rank; ws == 1: rBlock cuts, the last one grows):
+        # the packed range array is updated in place
+        loop_ends[:] = cur_end
         c2 = time.perf_counter()
-        step(rg=rg, mem=pb.MEM_HOST, qq=qh, oo=oh)
+        step(rg=loop_ra, mem=pb.MEM_HOST, qq=qh, oo=oh)
         c3 = time.perf_counter()
         brk[0] += c1 - c0
         brk[1] += c2 - c1
