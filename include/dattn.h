@@ -356,7 +356,8 @@ dattn_status dattn_ledger_advance(dattn_ledger* l, int64_t req, int64_t tokens);
 /* One decode step for n requests in order (ensure_step's loop,
  * simengine.cpp:356-371): ensure_slot for each, then advance by one token
  * every request that got a slot. instances[i] = the instance holding
- * request i's new token, or -1 (stalled, not advanced). */
+ * request i's new token, or -1 (stalled, not advanced). A request that is not
+ * live fails the call before the ledger changes. */
 dattn_status dattn_ledger_step(dattn_ledger* l, int n, const int64_t* reqs, int allow_borrow, int* instances);
 /* free_request on every instance (complete, simengine.cpp:300-303). */
 dattn_status dattn_ledger_release(dattn_ledger* l, int64_t req, int64_t* freed_blocks);

@@ -216,6 +216,7 @@ dattn_status dattn_ledger_step(dattn_ledger* l, int n, const int64_t* reqs, int 
     return guarded([&] {
         REQUIRE_ARG(l && (n == 0 || (reqs && instances)), "null argument");
         if (n < 0) throw Error(DATTN_ERR_CONTRACT, "ledger: negative request count");
+        for (int i = 0; i < n; ++i) (void)l->req(reqs[i]);  // all live before any change
         for (int i = 0; i < n; ++i) instances[i] = l->ensure_slot(reqs[i], allow_borrow != 0);
         for (int i = 0; i < n; ++i)
             if (instances[i] >= 0) l->req(reqs[i]).ctx += 1;

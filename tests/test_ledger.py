@@ -259,3 +259,13 @@ def test_batched_step_equals_slot_then_advance():
         assert got == want
     assert [a.segments(r) for r in reqs] == [b.segments(r) for r in reqs]
     assert [a.instance(j) for j in range(3)] == [b.instance(j) for j in range(3)]
+
+
+def test_batched_step_rejects_unknown_request_without_side_effects():
+    led = pb.Ledger([2, 8], 16)
+    assert led.admit(0, 0, 32)  # home full
+    before = (led.segments(0), led.instance(0), led.instance(1), led.borrowed())
+    with pytest.raises(pb.ContractError):
+        led.step([0, 99])
+    assert (led.segments(0), led.instance(0), led.instance(1), led.borrowed()) == before
+    assert led.step([0]) == [1]  # the slot is then borrowed on instance 1 as usual
