@@ -522,12 +522,19 @@ void dattn_store::build_plan(const dattn_batch& b, bool one_chunk_per_range, Pla
     // the chunk boundaries move (partition invariance).
     const dattn_range* R = b.ranges;
     std::vector<dattn_range> split;
-    // K2 runs one CTA per SM; quarter chunks below 1K tokens cost more per
-    // item than the shorter drain saves (measured: config 3 at N = 4, C = 2048:
-    // +2.4 us per step; C = 4096 / 8192: -8 / -17 us)
+    // K2 runs one CTA per SM. Chunks from 2048 tokens are cut (quarters of
+    // 512+ tokens): with K2 fetching its next item during the current one's
+    // last tiles, short items are cheap (config 3 at N = 4, C = 2048: -3.7 us
+    // per step; without that prefetch the same cut cost +2.4 us; C = 4096 /
+    // 8192: -8 / -17 us)
     const int64_t slots = static_cast<int64_t>(num_sms) * (tc_ok ? 1 : ma_ctas_per_sm);
     static const bool fine_tail_off = std::getenv("DATTN_NO_FINE_TAIL") != nullptr;  // A/B switch
-    if (!fine_tail_off && !one_chunk_per_range && b.chunk_tokens <= 0 && C >= 4096 &&
+    static const int64_t fine_tail_min = [] {  // smallest chunk cut into quarters (A/B: DATTN_FINE_TAIL_MIN)
+        const char* e = std::getenv("DATTN_FINE_TAIL_MIN");
+        return e ? std::max<int64_t>(64, std::atoll(e)) : int64_t{2048};
+    }();
+    if (!fine_tail_off && !one_chunk_per_range && b.chunk_tokens <= 0 &&
+        C >= (tc_ok ? fine_tail_min : std::max<int64_t>(fine_tail_min, 4096)) &&  // K1: no item prefetch
         C % (4 * cfg.page_tokens) == 0) {
         bool uniform = nr > 0;
         int64_t nh_sum = 0, natural = 0;
@@ -752,6 +759,11 @@ void dattn_store::run_ma(const Plan& pl, const void* q_dev, void* recs, double s
     p.nranges = pl.nranges;
     p.nitems = pl.nitems;
     p.chunk_tokens = pl.chunk_tokens;
+    static const int ahead = [] {  // DATTN_K2_AHEAD: A/B switch (0 = fetch at the item boundary)
+        const char* e = std::getenv("DATTN_K2_AHEAD");
+        return e ? std::max(0, std::atoi(e)) : 5;
+    }();
+    p.claim_ahead = ahead;
     const double s = scale > 0.0 ? scale : effective_scale();
     p.scale_log2 = s * 1.4426950408889634074;
     p.records = recs;

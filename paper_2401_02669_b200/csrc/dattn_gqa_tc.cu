@@ -68,7 +68,7 @@ struct Smem {
     uint64_t s_full, s_free;
     uint64_t p_full[2], o_full[2], o_free[2];
     TileMeta meta[kMeta];
-    int32_t pid[kPidWin];
+    int32_t pid[kPidWin];  // page ids of the current item's window
     float red_max[2][4][kN];
     float red_sum[4][kN];
     MergeQueue mq;  // completed groups -> merge warp
@@ -270,57 +270,121 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ================================ K producer
-        // The whole warp decodes each item and fetches its page ids into
-        // shared memory in one round trip; lane 0 publishes the tile
-        // descriptor and streams K (+ Q) tiles into the K ring.
+        // Lane 0 publishes the tile descriptors and streams K (+ Q) tiles
+        // into the K ring. The NEXT item is fetched during the current one's
+        // last tiles, one dependent step per tile (the producer mostly waits
+        // for ring slots): claim (atomic), claim-table entry, range + chunk
+        // prefix, the whole warp's page-id loads into registers; the ids go
+        // to shared memory at the boundary. An item boundary then costs no
+        // round trip, which matters for the short items of ragged batches,
+        // of fine tails and of the small per-GPU shares at N > 1. The claim is
+        // made only kAhead (5) tiles before the end, so a CTA never sits on an
+        // item another CTA could have started (the launch's tail).
         const uint64_t pol = l2_policy_evict_first();
-        uint32_t t = 0;  // global tile counter of this CTA
-        for (;;) {
-            int item = 0;
-            if (lane == 0) item = static_cast<int>(atomicAdd(p.work_counter, 1ull) - p.work_base);
-            item = __shfl_sync(0xffffffffu, item, 0);
-            if (item >= p.nitems) break;
-            int r, local;
-            if (p.item_table) {  // longest-first claim order (one load replaces the search)
-                const int2 e = __ldg(reinterpret_cast<const int2*>(p.item_table) + item);
-                r = e.x;
-                local = e.y;
-            } else {
-                r = find_item_range(p.item_prefix, p.nranges, item);
-                local = item - __ldg(p.item_prefix + r);
-            }
-            const RangeDev rg = p.ranges[r];
+        constexpr int kIdsPerLane = kPidWin / 32;
+        const int kAhead = p.claim_ahead;  // tiles before an item's end at which the next claim starts
+        struct Item {
+            int item, kvh, tlo, thi, gchunk, start, plast;
+            RangeDev rg;
+        };
+        // decode a claimed item from its (range, local) pair
+        auto decode = [&](Item& it, int r, int local, const RangeDev& rg, int cprefix) {
             const int nh = rg.kv_head < 0 ? p.num_kv_heads : 1;
             const int j = local / nh;
-            const int kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
-            const int tlo = rg.lo + j * p.chunk_tokens;
-            const int thi = min(rg.hi, tlo + p.chunk_tokens);
-            const int gchunk = __ldg(p.chunk_prefix + r) + j;
-            const int32_t* bt = p.block_tables + static_cast<int64_t>(rg.seq) * p.bt_stride;
-            const int start = (tlo / P) * P;
-            const int qrow = rg.out_row * p.num_q_heads + kvh * G;
-            const int plast = (thi - 1) / P;
-            int win = -1;  // first page id held in S.pid
-            for (int t0 = start; t0 < thi; t0 += kTile, ++t) {
-                const int tend = min(thi, t0 + kTile);
+            it.rg = rg;
+            it.kvh = rg.kv_head < 0 ? local - j * nh : rg.kv_head;
+            it.tlo = rg.lo + j * p.chunk_tokens;
+            it.thi = min(rg.hi, it.tlo + p.chunk_tokens);
+            it.gchunk = cprefix + j;
+            it.start = (it.tlo / P) * P;
+            it.plast = (it.thi - 1) / P;
+            (void)r;
+        };
+        // next-item pipeline state
+        int stage = 0;          // 0 idle, 1 claim issued, 2 entry loaded, 3 range loaded, 4 ids in registers, 5 ready
+        unsigned long long raw = 0;
+        int nitem = 0, nr = 0, nlocal = 0, ncp = 0;
+        int2 nentry = make_int2(0, 0);
+        RangeDev nrg{};
+        Item nxt{};
+        int nids[kIdsPerLane];
+        auto advance = [&]() {  // one dependent step of the next item's fetch
+            if (stage == 0) {
+                if (lane == 0) raw = atomicAdd(p.work_counter, 1ull);
+                stage = 1;
+            } else if (stage == 1) {
+                nitem = __shfl_sync(0xffffffffu, static_cast<int>(raw - p.work_base), 0);
+                if (nitem >= p.nitems) {
+                    stage = 5;
+                } else {
+                    if (p.item_table) nentry = __ldg(reinterpret_cast<const int2*>(p.item_table) + nitem);
+                    stage = 2;
+                }
+            } else if (stage == 2) {
+                if (p.item_table) {
+                    nr = nentry.x;
+                    nlocal = nentry.y;
+                } else {
+                    nr = find_item_range(p.item_prefix, p.nranges, nitem);
+                    nlocal = nitem - __ldg(p.item_prefix + nr);
+                }
+                nrg = p.ranges[nr];
+                ncp = __ldg(p.chunk_prefix + nr);
+                stage = 3;
+            } else if (stage == 3) {
+                decode(nxt, nr, nlocal, nrg, ncp);
+                nxt.item = nitem;
+                const int32_t* bt = p.block_tables + static_cast<int64_t>(nxt.rg.seq) * p.bt_stride;
+                const int w0 = nxt.start / P;
+#pragma unroll
+                for (int i = 0; i < kIdsPerLane; ++i) {
+                    const int k = i * 32 + lane;
+                    nids[i] = (w0 + k <= nxt.plast) ? __ldg(bt + w0 + k) : 0;
+                }
+                stage = 4;
+            } else if (stage == 4) {
+                stage = 5;  // stored at the item boundary (the buffer is in use until then)
+            }
+        };
+        auto finish = [&]() {  // complete the fetch synchronously
+            while (stage < 5) advance();
+        };
+
+        uint32_t t = 0;  // global tile counter of this CTA
+        finish();
+        while (nitem < p.nitems) {
+            // the prefetched item becomes current: its page ids into S.pid
+            const Item cur = nxt;
+#pragma unroll
+            for (int i = 0; i < kIdsPerLane; ++i) S.pid[i * 32 + lane] = nids[i];
+            __syncwarp();
+            int win = cur.start / P;  // first page id held in S.pid
+            stage = 0;
+            const int ntiles = (cur.thi - cur.start + kTile - 1) / kTile;
+            int k = 0;  // tile index within the item
+            const int qrow = cur.rg.out_row * p.num_q_heads + cur.kvh * G;
+            const int32_t* bt = p.block_tables + static_cast<int64_t>(cur.rg.seq) * p.bt_stride;
+            for (int t0 = cur.start; t0 < cur.thi; t0 += kTile, ++t) {
+                const int tend = min(cur.thi, t0 + kTile);
                 const int pg0 = t0 / P, npages = (tend - 1) / P - pg0 + 1;
-                if (win < 0 || pg0 + npages > win + kPidWin) {
+                if (pg0 + npages > win + kPidWin) {  // an unaligned item longer than the window
                     __syncwarp();
                     win = pg0;
                     for (int i = lane; i < kPidWin; i += 32)
-                        if (win + i <= plast) S.pid[i] = __ldg(bt + win + i);
+                        if (win + i <= cur.plast) S.pid[i] = __ldg(bt + win + i);
                     __syncwarp();
                 }
+                if (ntiles - k++ <= kAhead) advance();
                 if (lane == 0) {
                     TileMeta& md = S.meta[t % kMeta];
-                    md.item = item;
+                    md.item = cur.item;
                     md.tile0 = t0;
-                    md.tlo = tlo;
-                    md.thi = thi;
-                    md.flags = (t0 == start ? 1 : 0) | (t0 + kTile >= thi ? 2 : 0);
-                    md.row = rg.out_row;
-                    md.kvh = kvh;
-                    md.gchunk = gchunk;
+                    md.tlo = cur.tlo;
+                    md.thi = cur.thi;
+                    md.flags = (t0 == cur.start ? 1 : 0) | (t0 + kTile >= cur.thi ? 2 : 0);
+                    md.row = cur.rg.out_row;
+                    md.kvh = cur.kvh;
+                    md.gchunk = cur.gchunk;
                     md.npages = npages;
                     bool run = npages * P == kTile;  // a full tile of consecutive pages
                     for (int pg = 0; pg < npages; ++pg) {
@@ -336,11 +400,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sq = sk + kKVBytes;
                     if (run) {
                         // one box per 64-column half instead of two per page
-                        tma_load_4d(sk, &tm_k4, 0, 0, kvh, md.page[0], &S.kfull[ks], pol);
-                        tma_load_4d(sk + kHalf, &tm_k4, 64, 0, kvh, md.page[0], &S.kfull[ks], pol);
+                        tma_load_4d(sk, &tm_k4, 0, 0, cur.kvh, md.page[0], &S.kfull[ks], pol);
+                        tma_load_4d(sk + kHalf, &tm_k4, 64, 0, cur.kvh, md.page[0], &S.kfull[ks], pol);
                     } else {
                         for (int pg = 0; pg < npages; ++pg) {
-                            const int row0 = (md.page[pg] * p.num_kv_heads + kvh) * P;
+                            const int row0 = (md.page[pg] * p.num_kv_heads + cur.kvh) * P;
                             const int off = pg * P * 128;
                             tma_load_2d(sk + off, &tm_k, 0, row0, &S.kfull[ks], pol);
                             tma_load_2d(sk + kHalf + off, &tm_k, 64, row0, &S.kfull[ks], pol);
@@ -351,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
             }
+            finish();
         }
         if (lane == 0) {
             S.meta[t % kMeta].item = -1;

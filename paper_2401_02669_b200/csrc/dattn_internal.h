@@ -41,6 +41,7 @@ struct MAParams {
     unsigned long long work_base;      // counter value at this launch's start
     int32_t* nonfinite_flag;  // may be null
     int32_t stages;
+    int32_t claim_ahead;      // K2: tiles before an item's end at which the next item is fetched (0: at the boundary)
     // ---- fused group merge (K1 only; fused_mode 0 = records only) ----
     // 1: the CTA completing the last chunk of a (row, kv head) group merges the
     //    group's records into out_norm (and out_recs if set);
