@@ -363,12 +363,14 @@ def parity_check(w, out_host, lens, budget_tok_heads: float = 4e6):
 
 # ----------------------------------------------------------------- GPU side
 
-def kernel_code_sha256(lib_path: str):
+def kernel_code_sha256(lib_path: str, module: str = ""):
     """sha256 over the device code of a library: the .text.* (SASS) and
-    .nv.info* sections of every cubin embedded in it (cuobjdump -xelf all).
-    nvcc builds are not byte-reproducible -- the fatbin and the cubins' debug
-    line tables carry per-build temporary names -- but this code hash is, so a
-    capture stays valid across rebuilds of the same sources and nothing else."""
+    .nv.info* sections of every cubin embedded in it (cuobjdump -xelf all), or
+    of the cubins whose file name starts with ``module`` (e.g. "dattn_gqa_tc":
+    K2 alone). nvcc builds are not byte-reproducible -- the fatbin and the
+    cubins' debug line tables carry per-build temporary names -- but this code
+    hash is, so a capture stays valid across rebuilds of the same sources and
+    nothing else."""
     import struct
     with tempfile.TemporaryDirectory() as td:
         r = subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib_path)], cwd=td,
@@ -377,6 +379,8 @@ def kernel_code_sha256(lib_path: str):
             return None
         h = hashlib.sha256()
         for fn in sorted(os.listdir(td)):
+            if module and not fn.startswith(module):
+                continue
             b = open(os.path.join(td, fn), "rb").read()
             if b[:4] != b"\x7fELF" or b[4] != 2:
                 continue
@@ -408,7 +412,7 @@ def traffic_for(key: str):
         return None, "no capture"
     if not isinstance(ent, dict):
         return None, "no capture for this config"
-    code = kernel_code_sha256(pb.LIB_PATH)
+    code = kernel_code_sha256(pb.LIB_PATH, ent.get("code_module", ""))
     if code is None or ent.get("code_sha256") != code:
         return None, f"capture of other device code ({ent.get('git_head', '?')}); not reported"
     return ent.get("traffic"), f"ncu --set full, {ent.get('kernel')}, build {ent.get('git_head', '?')}"

@@ -50,6 +50,13 @@ sys.path.insert(0, ROOT)
 from bench import kernel_code_sha256  # noqa: E402
 
 
+def module_of(kernel: str) -> str:
+    """The cubin (source module) holding a kernel: K2 in dattn_gqa_tc, the
+    CUDA-core kernels in dattn_kernels. The stamp then covers that module's
+    device code only, so a change to another module leaves it valid."""
+    return "dattn_gqa_tc" if "gqa_tc_kernel" in kernel else "dattn_kernels"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("key")
@@ -75,7 +82,8 @@ def main():
     j[a.key] = {"traffic": sum(tr) / len(tr), "launches": len(tr), "kernel": sorted(names)[0],
                 "duration_ns": sum(dur) / len(dur) if dur else None,
                 "lib_sha256": hashlib.sha256(open(LIB, "rb").read()).hexdigest(),
-                "code_sha256": kernel_code_sha256(LIB),
+                "code_module": module_of(sorted(names)[0]),
+                "code_sha256": kernel_code_sha256(LIB, module_of(sorted(names)[0])),
                 "git_head": head, "report": os.path.basename(a.report),
                 "recorded": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
                 "metric": "dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)"}
