@@ -52,6 +52,7 @@ import gc
 import hashlib
 import json
 import os
+import shutil
 import socket
 import statistics
 import subprocess
@@ -373,8 +374,12 @@ def kernel_code_sha256(lib_path: str, module: str = ""):
     nothing else."""
     import struct
     with tempfile.TemporaryDirectory() as td:
-        r = subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib_path)], cwd=td,
-                           capture_output=True, text=True)
+        tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+        try:
+            r = subprocess.run([tool, "-xelf", "all", os.path.abspath(lib_path)], cwd=td,
+                               capture_output=True, text=True)
+        except OSError:
+            return None
         if r.returncode != 0:
             return None
         h = hashlib.sha256()
